@@ -1,0 +1,166 @@
+/*
+ * hcb.h -- C-ABI of libhcb.so, the B200 (sm_100a) IPGC hot path.
+ *
+ * The reference (hybridcolor, /root/reference/pkg) crosses into native code at
+ * exactly one place: the kernel-module plugin API that `_backend.get_kernels()`
+ * hands to the round functions (pkg/src/hybridcolor/_backend.py:13-44,
+ * _kernels.pyx:25-187).  The hc_k_* entry points below are that API, one per
+ * reference function, over DEVICE int64 buffers with the same argument meaning.
+ * hc_solve replaces the whole `color_graph` round loop
+ * (driver.py:122-176 + coloring.py:113-176 + worklist.py:77-91) with a single
+ * device-resident solve.  Graph construction / generation / verification
+ * entry points replace graph.py:184-201 and driver.py:179-204.
+ *
+ * Conventions (all entry points):
+ *   - plain pointers + sizes, no torch types;  `d_` pointers are device
+ *     pointers (borrowed for the duration of the call), `h_` are host.
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream).
+ *   - the library never allocates device memory: scratch comes from a
+ *     caller-owned workspace sized by the matching *_workspace_bytes query.
+ *   - return HC_OK (0) or a negative HC_ERR_* code; hc_last_error() gives the
+ *     message of the last failure on the calling host thread.
+ *   - one device per call (the caller selects it); reentrant per stream.
+ */
+#ifndef HCB_H_
+#define HCB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_OK 0
+#define HC_ERR_INVALID (-1)      /* bad argument (ValueError in the reference)        */
+#define HC_ERR_CUDA (-2)         /* CUDA runtime / launch failure                       */
+#define HC_ERR_WL_OVERFLOW (-3)  /* worklist overflow: worklist.py:50-58, 79-83         */
+#define HC_ERR_WORKSPACE (-4)    /* workspace too small                                 */
+#define HC_ERR_UNCOLORED (-5)    /* colors_used on a 0 entry: driver.py:183-184         */
+#define HC_ERR_DUPLICATE (-6)    /* duplicate push in one iteration: worklist.py:85-88  */
+#define HC_ERR_RECORDS (-7)      /* per-round record buffer too small (rounds returned) */
+
+#define HC_MODE_DATA 0   /* driver.py:149-150 */
+#define HC_MODE_TOPO 1   /* driver.py:147-148 */
+#define HC_MODE_HYBRID 2 /* driver.py:151-152 */
+
+/* One RoundRecord (driver.py:47-54); `topo` is mode_used == "topo". */
+typedef struct hc_round_rec {
+    int64_t round;
+    int64_t topo;
+    int64_t wl_in;
+    int64_t wl_out;
+    int64_t conflicts;
+    int64_t ns; /* device %globaltimer nanoseconds spent in the round */
+} hc_round_rec;
+
+const char *hc_last_error(void);
+int hc_version(void);
+/* number of SMs and the solver's resident CTAs per SM on the current device */
+int hc_device_info(int *h_num_sms, int *h_ctas_per_sm);
+
+/* ------------------------------------------------------------------ */
+/* Kernel-module plugin API (the reference's native operator surface). */
+/* All arrays int64 and C-contiguous on the device, exactly as in       */
+/* _kernels.pyx; `active` is uint8.  Scalar results are accumulated in  */
+/* the caller's device scalar d_acc (int64[1], zeroed by the call) and  */
+/* copied to the host pointer after the stream is synchronised.         */
+/* ------------------------------------------------------------------ */
+
+/* _kernels.pyx:29-58 assign_from_list */
+int hc_k_assign_from_list(const int64_t *d_row_offsets, const int64_t *d_col_indices,
+                          const int64_t *d_colors_read, int64_t *d_colors_write, int64_t *d_stamp,
+                          const int64_t *d_nodes, int64_t num_list, int64_t round_no,
+                          int64_t max_degree, void *stream);
+/* _kernels.pyx:61-91 assign_sweep; *h_processed = nodes with colors_read==0 */
+int hc_k_assign_sweep(const int64_t *d_row_offsets, const int64_t *d_col_indices,
+                      const int64_t *d_colors_read, int64_t *d_colors_write, int64_t *d_stamp,
+                      int64_t num_nodes, int64_t round_no, int64_t max_degree,
+                      int64_t *d_acc, int64_t *h_processed, void *stream);
+/* _kernels.pyx:94-120 resolve_from_list; *h_conflicts = sum of k_u */
+int hc_k_resolve_from_list(const int64_t *d_row_offsets, const int64_t *d_col_indices,
+                           const int64_t *d_colors_read, int64_t *d_colors_write,
+                           const int64_t *d_stamp, const int64_t *d_nodes, int64_t num_list,
+                           int64_t round_no, int64_t *d_next_ids, int64_t capacity,
+                           int64_t *d_cursor, int64_t *d_acc, int64_t *h_conflicts,
+                           void *stream);
+/* _kernels.pyx:123-149 resolve_sweep */
+int hc_k_resolve_sweep(const int64_t *d_row_offsets, const int64_t *d_col_indices,
+                       const int64_t *d_colors_read, int64_t *d_colors_write,
+                       const int64_t *d_stamp, int64_t num_nodes, int64_t round_no,
+                       int64_t *d_next_ids, int64_t capacity, int64_t *d_cursor,
+                       int64_t *d_acc, int64_t *h_conflicts, void *stream);
+/* _kernels.pyx:152-168 bench_from_list */
+int hc_k_bench_from_list(const int64_t *d_nodes, int64_t num_list, uint8_t *d_active,
+                         int64_t cutoff, int64_t *d_next_ids, int64_t capacity,
+                         int64_t *d_cursor, void *stream);
+/* _kernels.pyx:171-187 bench_sweep */
+int hc_k_bench_sweep(uint8_t *d_active, int64_t num_nodes, int64_t cutoff, int64_t *d_next_ids,
+                     int64_t capacity, int64_t *d_cursor, void *stream);
+
+/* Commits between phases, coloring.py:105-110:
+ *   _commit_list:    colors_read[nodes] = colors_write[nodes]
+ *   _commit_stamped: colors_read[u] = colors_write[u] where stamp[u] == round_no */
+int hc_k_commit_list(int64_t *d_colors_read, const int64_t *d_colors_write, const int64_t *d_nodes,
+                     int64_t num_list, void *stream);
+int hc_k_commit_stamped(int64_t *d_colors_read, const int64_t *d_colors_write,
+                        const int64_t *d_stamp, int64_t num_nodes, int64_t round_no, void *stream);
+
+/* Worklist.swap_and_sort (worklist.py:77-91): d_sorted[0..m) = ascending
+ * d_next[0..m) with m = *d_cursor; duplicate ids -> HC_ERR_DUPLICATE, m >
+ * capacity -> HC_ERR_WL_OVERFLOW.  *h_count = m.  Workspace: capacity+1 int64. */
+size_t hc_wl_sort_workspace_bytes(int64_t capacity);
+int hc_wl_swap_and_sort(const int64_t *d_next, const int64_t *d_cursor, int64_t capacity,
+                        int64_t *d_sorted, int64_t *h_count, void *d_ws, size_t ws_bytes,
+                        void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Device-resident solve (replaces the color_graph round loop).         */
+/* ------------------------------------------------------------------ */
+
+/* CSR: d_row_offsets int64[n+1], d_col_indices int32[m] (sorted, deduped,
+ * symmetric, loop-free as build_csr guarantees).  thr_count = ceil(H*n)
+ * computed by the host exactly as driver.py:138.  Output d_colors int64[n]
+ * (0 never appears on success).  d_rec receives up to max_rec round records;
+ * *h_rounds = total rounds.  If rounds > max_rec the solve still completes,
+ * the first max_rec records are kept and HC_ERR_RECORDS is returned. */
+size_t hc_solve_workspace_bytes(int64_t num_nodes, int64_t num_edges);
+int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+             int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
+             hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, void *d_ws,
+             size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Graph construction / generators / verification.                      */
+/* ------------------------------------------------------------------ */
+
+/* build_csr (graph.py:184-201) on device: d_edges int64[2*m] (src,dst pairs,
+ * all in [0,n)).  Outputs d_row_offsets int64[n+1] and d_col_indices int32
+ * with capacity 2*m; *h_num_edges = directed half-edges after symmetrise /
+ * drop loops / dedupe.  Workspace sized by hc_build_csr_workspace_bytes. */
+size_t hc_build_csr_workspace_bytes(int64_t num_nodes, int64_t num_pairs);
+int hc_build_csr(const int64_t *d_edges, int64_t num_pairs, int64_t num_nodes,
+                 int64_t *d_row_offsets, int32_t *d_col_indices, int64_t *h_num_edges,
+                 void *d_ws, size_t ws_bytes, void *stream);
+
+/* Synthetic edge streams (bit-identical to
+ * oracle/ipgc_oracle.c orc_gen_*).  d_edges int64[2*m]. */
+int hc_gen_grid(int64_t rows, int64_t cols, int64_t *d_edges, void *stream);
+int hc_gen_er(int64_t num_nodes, int64_t num_pairs, uint64_t seed, int64_t *d_edges, void *stream);
+int hc_gen_rmat(int scale, int64_t num_pairs, uint64_t seed, int64_t *d_edges, void *stream);
+
+/* verify_coloring (driver.py:188-204): *h_bad = #edges u<v with equal colors
+ * or colors[u]==0.  colors_used (driver.py:179-185): max color, 0 for n==0,
+ * HC_ERR_UNCOLORED if any entry < 1. */
+int hc_verify(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+              const int64_t *d_colors, int64_t *d_acc, int64_t *h_bad, void *stream);
+/* d_acc: int64[2] device scratch */
+int hc_colors_used(const int64_t *d_colors, int64_t num_nodes, int64_t *d_acc, int64_t *h_used,
+                   void *stream);
+/* int64 -> int32 column conversion for uploads of reference CsrGraph arrays */
+int hc_narrow_i64_i32(const int64_t *d_in, int32_t *d_out, int64_t count, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HCB_H_ */

@@ -1,0 +1,86 @@
+"""Per-round IPGC operations on device state (pkg/src/hybridcolor/coloring.py).
+
+`ColorState` (coloring.py:37-52) keeps the reference's double-buffered int64
+colors plus stamps, as CUDA tensors.  `data_driven_iteration` (113-142) and
+`topology_driven_iteration` (145-176) run one round through the `cuda`
+kernel module with the reference's commits (105-110) and worklist swap.
+This is the per-round path (golden round traces, plugin parity); the solve
+itself (`color_graph`) fuses all rounds into one device-resident kernel.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from . import kernels as cuda_kernels
+from .graph import CsrGraph, DeviceCsr
+from .worklist import Worklist
+
+
+@dataclass
+class ColorState:
+    colors_read: torch.Tensor
+    colors_write: torch.Tensor
+    active_stamp: torch.Tensor
+
+    @classmethod
+    def fresh(cls, num_nodes: int) -> "ColorState":
+        dev = _lib.device()
+        z = lambda: torch.zeros(num_nodes, dtype=torch.int64, device=dev)  # noqa: E731
+        return cls(colors_read=z(), colors_write=z(), active_stamp=z())
+
+
+@dataclass
+class RoundOutcome:
+    colored_permanently: int
+    pushed_back: int
+    conflicts_detected: int
+
+
+def _graph_arrays(graph):
+    if isinstance(graph, CsrGraph):
+        graph = graph.to_device()
+    if not isinstance(graph, DeviceCsr):
+        raise TypeError("expected CsrGraph or DeviceCsr")
+    return graph.row_offsets, graph.col_indices_i64, graph.max_degree
+
+
+def _kmod(kernels):
+    if kernels is not None and kernels is not cuda_kernels:
+        raise ValueError("only the cuda kernel module is available")
+    return cuda_kernels
+
+
+def data_driven_iteration(graph, state: ColorState, wl: Worklist, round_no: int, *,
+                          workers: int = 1, chunk_size: int = 1024, kernels=None) -> RoundOutcome:
+    """coloring.py:113-142"""
+    k = _kmod(kernels)
+    ro, ci, maxdeg = _graph_arrays(graph)
+    nodes = wl.current
+    k.assign_from_list(ro, ci, state.colors_read, state.colors_write, state.active_stamp,
+                       nodes, round_no, maxdeg, workers, chunk_size)
+    k.commit_list(state.colors_read, state.colors_write, nodes)
+    conflicts = k.resolve_from_list(ro, ci, state.colors_read, state.colors_write, state.active_stamp,
+                                    nodes, round_no, wl.next_storage, wl.cursor, workers, chunk_size)
+    k.commit_list(state.colors_read, state.colors_write, nodes)
+    n_in = int(nodes.numel())
+    pushed = wl.swap_and_sort()
+    return RoundOutcome(n_in - pushed, pushed, int(conflicts))
+
+
+def topology_driven_iteration(graph, state: ColorState, wl: Worklist, round_no: int, *,
+                              workers: int = 1, chunk_size: int = 1024, kernels=None) -> RoundOutcome:
+    """coloring.py:145-176"""
+    k = _kmod(kernels)
+    ro, ci, maxdeg = _graph_arrays(graph)
+    processed = k.assign_sweep(ro, ci, state.colors_read, state.colors_write, state.active_stamp,
+                               round_no, maxdeg, workers, chunk_size)
+    k.commit_stamped(state.colors_read, state.colors_write, state.active_stamp, round_no)
+    conflicts = k.resolve_sweep(ro, ci, state.colors_read, state.colors_write, state.active_stamp,
+                                round_no, wl.next_storage, wl.cursor, workers, chunk_size)
+    k.commit_stamped(state.colors_read, state.colors_write, state.active_stamp, round_no)
+    pushed = wl.swap_and_sort()
+    return RoundOutcome(int(processed) - pushed, pushed, int(conflicts))
