@@ -1,0 +1,424 @@
+"""Benchmark: edges/sec per IPGC solve (BASELINE.json metric), hybrid vs
+data-driven vs topology-driven, on the BASELINE configs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config grid4096]
+                    [--impl ours|reference]
+
+A step = one complete hybrid IPGC solve (hc_solve: bin preprocessing + the
+device-resident round loop) of the config's graph, inputs resident in HBM.
+L2 is flushed between timed steps (a 512 MiB write, outside the events).
+value = num_undirected_edges * steps / (sum of per-step CUDA-event times),
+max over ranks.  e2e = the same metric through the public drop-in API
+`color_graph(CsrGraph on pinned host memory)`: H2D of the CSR, solve, D2H of
+the colors, device verification.  `--impl reference` times the reference's own
+CPU implementation (oracle/_ref: hybridcolor with its compiled Cython/OpenMP
+backend) on the same graph -- see cpu_sample() for the bounded-sample rule.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "rmat16": dict(kind="rmat", scale=16, edgefactor=16, seed=0),
+    "grid4096": dict(kind="grid", rows=4096, cols=4096),
+    "rmat22": dict(kind="rmat", scale=22, edgefactor=16, seed=0),
+    "er25": dict(kind="er", n=1 << 25, avg_degree=32, seed=0),
+    "rmat26": dict(kind="rmat", scale=26, edgefactor=16, seed=0),
+}
+DESCRIPTIONS = {
+    "rmat16": "RMAT scale-16 edgefactor-16 undirected, seed 0 (configs[0])",
+    "grid4096": "2D grid 4096x4096 4-neighbor (configs[1])",
+    "rmat22": "RMAT scale-22 edgefactor-16, seed 0 (configs[2])",
+    "er25": "Erdos-Renyi 2^25 nodes avg degree 32, seed 0 (configs[3])",
+    "rmat26": "RMAT scale-26 edgefactor-16, seed 0 (configs[4])",
+}
+METRIC = "edges/sec per IPGC solve (hybrid)"
+UNIT = "undirected_edges/s"
+
+
+def peaks():
+    try:
+        return json.loads((REPO / "MEASURED_PEAKS.json").read_text())["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------------------
+# algorithmic byte model: per round t, W = processed nodes,
+# E = sum of their degrees, El = lower-id neighbours scanned by resolve
+#   assign : data 16|W| + 8E          topo 4n_sweep + 12|W| + 8E
+#   resolve: data 20|W| + 8El         topo 4n_sweep + 16|W| + 8El
+# (4 B list entry, 8 B row offset, 4 B X write / X read / push, 4+4 B per edge)
+# --------------------------------------------------------------------------
+def algorithmic_bytes(records: np.ndarray, stats: np.ndarray, n: int) -> int:
+    total = 0
+    for r, (ea, er) in zip(records, stats):
+        topo, w = int(r[1]), int(r[2])
+        if topo:
+            total += 4 * n + 12 * w + 8 * int(ea) + 4 * n + 16 * w + 8 * int(er)
+        else:
+            total += 16 * w + 8 * int(ea) + 20 * w + 8 * int(er)
+    return total
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# CPU side: the reference's own implementation on the host cores
+# --------------------------------------------------------------------------
+def host_csr(cfg):
+    """The config's graph built on the CPU by the oracle (test infrastructure;
+    bit-identical to the device build and to the reference build_csr, see
+    tests/test_oracle.py + tests/test_gpu_parity.py)."""
+    from oracle import oracle as O
+
+    if cfg["kind"] == "grid":
+        n = cfg["rows"] * cfg["cols"]
+        e = O.gen_grid(cfg["rows"], cfg["cols"])
+    elif cfg["kind"] == "er":
+        n = cfg["n"]
+        e = O.gen_er(n, n * cfg["avg_degree"] // 2, cfg["seed"])
+    else:
+        n = 1 << cfg["scale"]
+        e = O.gen_rmat(cfg["scale"], cfg["edgefactor"], cfg["seed"])
+    ro, ci = O.build_csr(n, e)
+    return n, ro, ci
+
+
+def cpu_sample(ref, g, budget_s: float, full_visits: int | None):
+    """Run the reference's hybrid loop (driver.py:143-169, through its public
+    data_driven_iteration / topology_driven_iteration) on the host for at most
+    `budget_s` seconds.  If the solve finishes, the rate is exact; otherwise the
+    full-solve time is extrapolated from the node-visit rate of the sampled
+    rounds: T_full = T_sample * sum_t|W_t| (whole solve, known from the
+    bit-identical GPU trajectory) / sum_{t<=R}|W_t| (sampled)."""
+    workers = os.cpu_count() or 1
+    cfgr = ref.HybridConfig(mode="hybrid", workers=workers)
+    n = g.num_nodes
+    thr = math.ceil(cfgr.threshold_fraction * n)
+    state = ref.ColorState.fresh(n)
+    wl = ref.Worklist.init_full(n)
+    round_no, visits, t_loop = 1, 0, 0.0
+    t0 = time.perf_counter()
+    while len(wl.current) > 0:
+        size_in = len(wl.current)
+        it = ref.topology_driven_iteration if size_in > thr else ref.data_driven_iteration
+        ts = time.perf_counter()
+        it(g, state, wl, round_no, workers=workers, chunk_size=cfgr.chunk_size)
+        t_loop += time.perf_counter() - ts
+        visits += size_in
+        round_no += 1
+        if time.perf_counter() - t0 > budget_s:
+            break
+    finished = len(wl.current) == 0
+    if finished:
+        secs = t_loop
+        sample = f"full hybrid solve ({round_no - 1} rounds)"
+    else:
+        if not full_visits:
+            return None
+        secs = t_loop * full_visits / visits
+        sample = (f"first {round_no - 1} rounds of the hybrid solve ({visits} of {full_visits} node-visits), "
+                  f"extrapolated by node-visit rate")
+    return {"value": (g.num_edges // 2) / secs, "unit": UNIT, "cores": workers, "kind": "reference",
+            "sample": sample, "solve_seconds": secs, "finished": finished}
+
+
+def reference_module():
+    from oracle import oracle as O
+
+    ref = O.reference_module()
+    if ref is None:
+        raise RuntimeError("oracle/_ref missing: run oracle/build_ref.sh in the build container")
+    assert "cython" in ref.available_backends()
+    return ref
+
+
+def warm_reference(ref):
+    g = ref.build_csr(ref.EdgeList(64, np.column_stack([np.arange(63), np.arange(1, 64)])))
+    ref.color_graph(g, ref.HybridConfig(workers=os.cpu_count() or 1))
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    ref = reference_module()
+    warm_reference(ref)
+    n, ro, ci = host_csr(cfg)
+    g = ref.CsrGraph(n, len(ci), ro, ci)
+    full_visits = known_visits(args.config)
+    steps = max(1, args.steps)
+    per_step = min(30.0, max(5.0, 150.0 / (steps + args.warmup)))
+    for _ in range(args.warmup):
+        cpu_sample(ref, g, per_step / 3, full_visits)
+    vals = []
+    last = None
+    for _ in range(steps):
+        last = cpu_sample(ref, g, per_step, full_visits)
+        vals.append(last["value"])
+    value = float(statistics.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": (g.num_edges // 2) / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C)",
+        "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": "hybrid",
+                   "num_nodes": n, "num_undirected_edges": len(ci) // 2},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": last["cores"], "kind": "reference",
+                         "sample": last["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def known_visits(config):
+    """sum_t |W_t| of the full solve, for configs whose trajectory is known in
+    closed form (grid: the wavefront colors the anti-diagonals; measured on
+    the GPU and pinned by tests) -- else None (filled in from the GPU run)."""
+    p = REPO / "profiles" / f"visits_{config}.json"
+    if p.exists():
+        return json.loads(p.read_text())["sum_wl_in"]
+    return None
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+def build_graph(hc, cfg):
+    if cfg["kind"] == "grid":
+        return hc.grid_graph(cfg["rows"], cfg["cols"])
+    if cfg["kind"] == "er":
+        return hc.er_graph(cfg["n"], cfg["avg_degree"], cfg["seed"])
+    return hc.rmat_graph(cfg["scale"], cfg["edgefactor"], cfg["seed"])
+
+
+def run_ours(args, cfg):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_01478_b200 as hc
+    from paper_1912_01478_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    dg = build_graph(hc, cfg)
+    torch.cuda.synchronize()
+    n, und = dg.num_nodes, dg.num_undirected_edges
+    hcfg = hc.HybridConfig(mode=args.mode)
+    thr = hc.threshold_count(hcfg, n)
+    solver = hc.Solver(dg)
+    L = _lib.load()
+
+    # one instrumented solve (outside the timed region) for the byte model
+    stats = torch.zeros((solver.max_rec, 2), dtype=torch.int64, device=dev)
+    rounds = ctypes.c_int64(0)
+    _lib.check(L.hc_solve_stats(dg.row_offsets.data_ptr(), _lib.ptr(dg.col_indices), n, dg.num_edges,
+                                _lib.MODE_CODES[args.mode], thr, solver.colors.data_ptr(),
+                                solver.rec.data_ptr(), solver.max_rec, ctypes.byref(rounds),
+                                stats.data_ptr(), solver.ws.data_ptr(), solver.ws.numel(),
+                                _lib.stream_handle()))
+    R = int(rounds.value)
+    recs = solver.rec[:R].cpu().numpy()
+    st = stats[:R].cpu().numpy()
+    b_alg = algorithmic_bytes(recs, st, n)
+    sum_visits = int(recs[:, 2].sum())
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        solver.run(args.mode, thr, fetch_records=False)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stream = torch.cuda.current_stream()
+    launches_per_step = 5  # partition count/scan/write + copy_totals + solve_kernel
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps, outside the events
+            starts[i].record(stream)
+            rc = L.hc_solve(dg.row_offsets.data_ptr(), _lib.ptr(dg.col_indices), n, dg.num_edges,
+                            _lib.MODE_CODES[args.mode], thr, solver.colors.data_ptr(),
+                            solver.rec.data_ptr(), solver.max_rec, ctypes.byref(rounds),
+                            solver.ws.data_ptr(), solver.ws.numel(), _lib.stream_handle(stream))
+            stops[i].record(stream)
+            _lib.check(rc)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * und * args.steps / (total_ms / 1e3)
+    clocks = clk.summary()
+
+    # hybrid vs the GPU's own pure data / topology modes (untimed for the headline)
+    modes = {}
+    if not args.skip_modes:
+        for mode in ("hybrid", "data", "topo"):
+            ts = []
+            for _ in range(3):
+                flush.zero_()
+                ts.append(solver.run(mode, thr, fetch_records=False).seconds)
+            modes[mode] = {"ms": min(ts) * 1e3, "und_edges_per_s": und / min(ts)}
+        modes["hybrid_speedup_vs_data"] = modes["data"]["ms"] / modes["hybrid"]["ms"]
+        modes["hybrid_speedup_vs_topo"] = modes["topo"]["ms"] / modes["hybrid"]["ms"]
+
+    # e2e through the public API on pinned host buffers
+    host = dg.to_host()
+    pinned = hc.CsrGraph.pinned(host)
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        colors, rep = hc.color_graph(pinned, hcfg)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert rep.valid
+    e2e_total = float(sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    e2e_value = world * und * args.steps / (e2e_total / 1e3)
+
+    hbm, peak_kind = peaks()
+    achieved = b_alg / (ms_per_step / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPU",
+        "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": args.mode,
+                   "num_nodes": n, "num_undirected_edges": und, "rounds": R,
+                   "sum_wl_in": sum_visits, "l2": "flushed between timed steps (512 MiB write)",
+                   "parallelism": "replicas" if world > 1 else "single-gpu"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "solve_kernel (+ bin preprocessing, whole hc_solve step)",
+                     "algorithmic_bytes_per_launch": b_alg},
+        "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+        "modes": modes,
+        "e2e": {"value": e2e_value, "unit": UNIT,
+                "h2d_bytes_per_step": 8 * (n + 1) + 8 * dg.num_edges,
+                "d2h_bytes_per_step": 8 * n + 48 * R, "ms_per_step": e2e_total / args.steps},
+        "step_ms": step_ms,
+    }
+    if rank == 0 and world == 1 and not args.skip_cpu:
+        try:
+            ref = reference_module()
+            warm_reference(ref)
+            g = ref.CsrGraph(host.num_nodes, host.num_edges, host.row_offsets, host.col_indices)
+            line["cpu_baseline"] = cpu_sample(ref, g, args.cpu_budget, sum_visits)
+        except Exception as exc:  # reported, not fatal
+            line["cpu_baseline"] = {"value": None, "unavailable": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="grid4096")
+    ap.add_argument("--mode", choices=("hybrid", "data", "topo"), default="hybrid")
+    ap.add_argument("--skip-modes", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -130,6 +130,15 @@ int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t
              hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, void *d_ws,
              size_t ws_bytes, void *stream);
 
+/* hc_solve plus per-round edge-visit statistics (for the roofline's
+ * algorithmic byte count): d_stats int64[2*max_rec], round t (1-based) gets
+ * d_stats[2(t-1)] = sum of degrees over nodes assigned in round t and
+ * d_stats[2(t-1)+1] = lower-id neighbours scanned by resolve in round t. */
+int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                   int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
+                   hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, int64_t *d_stats,
+                   void *d_ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Graph construction / generators / verification.                      */
 /* ------------------------------------------------------------------ */

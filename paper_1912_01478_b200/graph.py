@@ -78,14 +78,33 @@ class CsrGraph:
     def neighbors(self, u: int) -> np.ndarray:
         return self.col_indices[self.row_offsets[u] : self.row_offsets[u + 1]]
 
+    @classmethod
+    def pinned(cls, g: "CsrGraph") -> "CsrGraph":
+        """Copy of `g` whose arrays live in page-locked host memory, so uploads
+        are straight DMA (no staging copy)."""
+        ro = torch.from_numpy(np.array(g.row_offsets)).pin_memory()
+        ci = torch.from_numpy(np.array(g.col_indices)).pin_memory()
+        out = cls(g.num_nodes, g.num_edges, ro.numpy(), ci.numpy())
+        out._pinned = (ro, ci)
+        return out
+
+    def _host_tensors(self):
+        pinned = getattr(self, "_pinned", None)
+        if pinned is not None:
+            return pinned
+        ro = torch.from_numpy(np.array(self.row_offsets)).pin_memory()
+        ci = torch.from_numpy(np.array(self.col_indices)).pin_memory()
+        return ro, ci
+
     def to_device(self, dev: torch.device | None = None) -> "DeviceCsr":
-        """Upload (pinned staging) and narrow the column ids to int32 on the GPU."""
+        """Upload (pinned host memory) and narrow the column ids to int32 on the GPU."""
         dev = dev or _lib.device()
         n, m = self.num_nodes, self.num_edges
-        ro = torch.from_numpy(np.asarray(self.row_offsets)).pin_memory().to(dev, non_blocking=True)
+        h_ro, h_ci = self._host_tensors()
+        ro = h_ro.to(dev, non_blocking=True)
         ci32 = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
         if m:
-            ci64 = torch.from_numpy(np.asarray(self.col_indices)).pin_memory().to(dev, non_blocking=True)
+            ci64 = h_ci[:m].to(dev, non_blocking=True)
             _lib.check(_lib.load().hc_narrow_i64_i32(ci64.data_ptr(), ci32.data_ptr(), m,
                                                       _lib.stream_handle()))
             del ci64
