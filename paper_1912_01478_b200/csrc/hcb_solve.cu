@@ -29,23 +29,32 @@
 //     still count for higher neighbours (test_coloring.py:84-91).
 //   * winners commit C[u]=T[u] in resolve itself; no separate commit pass.
 //
-// Work distribution (IrGL-style nested parallelism):
-// nodes are binned once by degree -- small (thread per node, NPT nodes per
-// thread with all their loads batched for memory-level parallelism), mid
-// (warp per node; CTA per node in rounds with few active mid nodes, where
-// latency rather than throughput decides), hub (CTA per node).  The
-// always-maintained worklist is kept per bin and double buffered.  Each phase
-// hands out units with ONE atomic per unit: hub nodes first (largest work
-// first), then chunks of mid nodes, then chunks of small nodes.  Losers of
-// chunk c are compacted (order-preserving for the small bin) into output
-// segment c of the next worklist and the chunk writes its loser count; the
-// next round rebuilds the segment prefix in shared memory.  So pushes need no
-// global atomics, the worklist stays sorted by id (segments are in chunk
-// order), and topology-driven rounds (static bin lists + activity test) and
-// data-driven rounds (segmented dynamic lists) share the same code.
+// Work distribution (IrGL-style nested parallelism).
+// Nodes are binned once by degree; each bin has its own granularity:
+//   bin 0  deg <= 16        one thread per node, NPT=4 nodes per thread with
+//                           all their loads batched (memory-level parallelism)
+//   bin 1  17..32           a group of 8 lanes per node (4 nodes per warp)
+//   bin 2  33..64           16 lanes per node (2 per warp)
+//   bin 3  65..4096         one warp per node; one CTA per node in rounds with
+//                           few active bin-3 nodes (latency regime)
+//   bin 4  > 4096 (hubs)    one CTA per node
+// Within a group every lane issues 4 neighbour loads before consuming any.
+// The mex is first taken over a 64-bit register mask of colors 1..64 (OR-
+// reduced across the group); only nodes whose colors 1..64 are all taken fall
+// back to a shared-memory bitmap window.
+// The always-maintained worklist is kept per bin and double buffered.  Each
+// phase hands out units with ONE atomic per unit: hubs first (largest work
+// first), then chunks of bins 3, 2, 1, 0.  Losers of chunk c are compacted
+// into output segment c of the next worklist (order-preserving for bin 0) and
+// the chunk writes its loser count; the next round rebuilds the segment prefix
+// in shared memory.  So pushes need no global atomics, the worklist stays
+// (nearly) sorted by id, and topology-driven rounds (static bin lists +
+// activity test) and data-driven rounds (segmented dynamic lists) share the
+// same code.
 //
 // Row offsets are read as int32 when num_edges < 2^31 (a copy made in the
-// preprocessing), halving the offset traffic; int64 otherwise.
+// preprocessing), halving the offset traffic; int64 otherwise.  Column loads
+// are streaming (evict-first) so the X gathers keep L2.
 #include <algorithm>
 
 #include "hcb_partition.cuh"
@@ -55,16 +64,20 @@ namespace solve {
 
 constexpr int BLOCK = 1024;
 constexpr int NW = BLOCK / 32;
-constexpr int NPT = 4;                   // small nodes per thread per tile
-constexpr int SMALL_MAX = 16;            // deg <= SMALL_MAX : thread per node (64-bit mask mex)
-constexpr int MID_WORDS = 64;            // warp bitmap words -> mid nodes up to 2046 neighbours
-constexpr int MID_MAX = MID_WORDS * 32 - 2;
+constexpr int NPT = 4;                   // bin-0 nodes per thread per tile
+constexpr int NSEG_BINS = 4;             // bins 0..3 are segmented; bin 4 (hubs) is dense
+constexpr int BIN_HUB = 4;
+constexpr int NBIN = 5;
+constexpr int HUB_MIN = 4097;            // deg >= HUB_MIN -> hub
 constexpr int HUB_WORDS = 512;           // CTA bitmap window: 16384 colors per pass
+constexpr int WIN_WORDS = 32;            // warp bitmap window: 1024 colors per pass
 constexpr int MAXSEG = 2048;             // output segments per bin per round
 constexpr unsigned FBIT = 0x80000000u;
 constexpr unsigned CMASK = 0x7fffffffu;
 
-enum { BIN_SMALL = 0, BIN_MID = 1, BIN_HUB = 2, NBIN = 3 };
+__host__ __device__ constexpr int bin_of_degree(long long d) {
+    return d <= 16 ? 0 : d <= 32 ? 1 : d <= 64 ? 2 : d < HUB_MIN ? 3 : 4;
+}
 
 struct Ctrl {
     GridBarrier bar;
@@ -76,7 +89,7 @@ struct Ctrl {
     unsigned int unit_ctr[2][2];                 // [phase][parity]
     long long rounds;
     long long rec_overflow;
-    unsigned segcnt[2][2][MAXSEG];               // [parity][small|mid][segment] loser counts
+    unsigned segcnt[2][NSEG_BINS][MAXSEG];       // [parity][bin][segment] loser counts
 };
 
 struct Params {
@@ -84,7 +97,7 @@ struct Params {
     const int *ci;
     long long n;
     unsigned *X;
-    int *stat;                 // static lists, bins contiguous (small | mid | hub)
+    int *stat;                 // static lists, bins contiguous
     int *dyn[2][NBIN];         // dynamic lists per parity and bin
     Ctrl *ctrl;
     hc_round_rec *rec;
@@ -111,15 +124,16 @@ struct RoundCfg {
     List L[NBIN];
     const int *stat_lists[NBIN];
     unsigned long long nst[NBIN];
-    unsigned csz0, csz1, nch0, nch1, n_hub, units;
-    unsigned prev_nseg[2], prev_cap[2];
-    bool topo, ident, mid_by_cta, ident_small;
+    unsigned csz[NSEG_BINS], nch[NSEG_BINS];
+    unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
+    unsigned prev_nseg[NSEG_BINS], prev_cap[NSEG_BINS];
+    bool topo, ident, bin3_by_cta, ident_small;
 };
 
 struct Smem {
     RoundCfg rc;
-    unsigned prefix[2][MAXSEG + 1];   // segment prefix of the current small / mid lists
-    unsigned mid_bm[NW][MID_WORDS];
+    unsigned prefix[NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
+    unsigned win_bm[NW][WIN_WORDS];
     unsigned hub_bm[HUB_WORDS];
     unsigned warp_tmp[NPT * NW];
     unsigned long long red;
@@ -151,78 +165,128 @@ __device__ __forceinline__ void mark(unsigned *bm, unsigned c) {
     atomicOr(&bm[(c - 1u) >> 5], 1u << ((c - 1u) & 31u));
 }
 
-// ------------------------------------------------------------------ mid (warp)
-template <typename OffT>
-__device__ __forceinline__ unsigned assign_mid(const Params &P, const OffT *ro, int u, unsigned *bm,
-                                               unsigned &deg_out) {
-    const unsigned lane = lane_id();
-    const long long b = ro[u], e = ro[u + 1];
-    const unsigned lim = (unsigned)(e - b) + 1u;  // mex <= deg+1 (_kernels.pyx:49)
-    deg_out = lim - 1u;
-#pragma unroll
-    for (int w = 0; w < MID_WORDS / 32; ++w) bm[lane + 32 * w] = 0u;
-    __syncwarp();
-    for (long long k = b + lane; k < e; k += 128) {
-        int v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = (k + 32 * q < e) ? P.ci[k + 32 * q] : -1;
-        unsigned x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? P.X[v[q]] : 0u;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const unsigned c = x[q] & CMASK;
-            if ((x[q] & FBIT) && c <= lim) mark(bm, c);
-        }
-    }
-    __syncwarp();
-    unsigned T = 0;
-#pragma unroll
-    for (int w = 0; w < MID_WORDS / 32; ++w) {
-        const unsigned word = bm[lane + 32 * w];
-        const unsigned bal = __ballot_sync(FULL, word != FULL);
-        if (bal) {
-            const int f = __ffs(bal) - 1;
-            const unsigned fw = __shfl_sync(FULL, word, f);
-            T = (unsigned)((w * 32 + f) * 32 + __ffs(~fw));
-            break;
-        }
-    }
-    __syncwarp();
-    return T;
+// streaming load of a column id: evict-first so the X gathers keep L2
+__device__ __forceinline__ int ld_col(const int *p) { return __ldcs(p); }
+
+__device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
+    const unsigned c = x & CMASK;
+    if ((x & FBIT) && c <= 64u) mask |= 1ull << (c - 1u);
 }
 
-template <typename OffT>
-__device__ __forceinline__ unsigned resolve_mid(const Params &P, const OffT *ro, int u, unsigned T,
-                                                unsigned &lower_out) {
+// ------------------------------------------------------------------ groups
+// Warp-level mex over window(s) above color 64, for a node whose colors
+// 1..64 are all taken (rare): whole warp, one node.
+__device__ unsigned warp_mex_above64(const Params &P, long long b, long long e, unsigned *bm) {
     const unsigned lane = lane_id();
-    const long long b = ro[u], e = ro[u + 1];
-    unsigned cnt = 0, low = 0;
-    for (long long k0 = b; k0 < e; k0 += 128) {
-        int v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const long long k = k0 + 32 * q + lane;
-            v[q] = k < e ? P.ci[k] : 0x7fffffff;
+    const unsigned lim = (unsigned)(e - b) + 1u;
+    for (unsigned w0 = 64;; w0 += WIN_WORDS * 32) {
+        bm[lane] = 0u;
+        __syncwarp();
+        const unsigned hi = min(lim, w0 + WIN_WORDS * 32);
+        for (long long k = b + lane; k < e; k += 32) {
+            const unsigned x = P.X[ld_col(P.ci + k)];
+            const unsigned c = x & CMASK;
+            if ((x & FBIT) && c > w0 && c <= hi) mark(bm, c - w0);
         }
-        unsigned x[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[q] < u ? P.X[v[q]] : 0u;
-        bool stop = false;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (v[q] < u) { cnt += (x[q] & CMASK) == T; ++low; }
-            else stop = true;
+        __syncwarp();
+        const unsigned word = bm[lane];
+        const unsigned bal = __ballot_sync(FULL, word != FULL);
+        __syncwarp();
+        if (bal) {
+            const int f = __ffs(bal) - 1;
+            return w0 + (unsigned)f * 32u + (unsigned)__ffs(~__shfl_sync(FULL, word, f));
         }
-        if (__any_sync(FULL, stop)) break;  // adjacency sorted: the rest is >= u
     }
-    lower_out = warp_sum(low);
-    return warp_sum(cnt);
+}
+
+// One warp tile of a group bin: 32/G nodes, G lanes per node.
+template <int G, typename OffT, bool STATS, int PHASE>
+__device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, const List &L,
+                                           const unsigned *prefix, unsigned long long v0,
+                                           unsigned long long hi, bool topo, int *out,
+                                           unsigned *out_cnt, unsigned *bm,
+                                           unsigned long long &my_conf, unsigned long long *my_edges) {
+    const unsigned lane = lane_id();
+    const unsigned sub = lane % G, gi = lane / G;
+    const unsigned long long v = v0 + gi;
+    int u = v < hi ? L.base[list_index(L, prefix, v)] : -1;
+    unsigned xu = 0;
+    if (topo || PHASE == 1) {
+        xu = u >= 0 ? P.X[u] : 0u;
+        if (topo && (xu & FBIT)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
+    }
+    const long long b = u >= 0 ? (long long)ro[u] : 0, e = u >= 0 ? (long long)ro[u + 1] : 0;
+    unsigned iters = (unsigned)((e - b + 4 * G - 1) / (4 * G));
+    iters = __reduce_max_sync(FULL, iters);
+    unsigned long long mask = 0;
+    unsigned cnt = 0, low = 0;
+    bool stop = u < 0;
+    for (unsigned it = 0; it < iters; ++it) {
+        const long long kb = b + (long long)it * 4 * G + sub;
+        int nb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long k = kb + q * G;
+            nb[q] = (!stop && k < e) ? ld_col(P.ci + k) : (PHASE == 0 ? -1 : 0x7fffffff);
+        }
+        if (PHASE == 0) {
+            unsigned x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = nb[q] >= 0 ? P.X[nb[q]] : 0u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mask_add(mask, x[q]);
+        } else {
+            unsigned x[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = nb[q] < u ? P.X[nb[q]] : 0u;
+            bool ge = false;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (nb[q] < u) { cnt += (x[q] & CMASK) == xu; ++low; }
+                else if (nb[q] != 0x7fffffff) ge = true;
+            }
+            // adjacency sorted ascending (graph.py:193-197): once any lane of the
+            // group saw a neighbour >= u, the group's later iterations are all >= u
+            const unsigned bal = __ballot_sync(FULL, ge);
+            const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (gi * G));
+            if (bal & gmask) stop = true;
+            if (__all_sync(FULL, stop)) break;
+        }
+    }
+    if (PHASE == 0) {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) mask |= __shfl_xor_sync(FULL, mask, o);
+        unsigned T;
+        if (mask != ~0ull) {
+            T = (unsigned)__ffsll((long long)~mask);
+        } else if (G < 32) {
+            T = 65u;  // deg <= 64 and colors 1..64 all taken: exactly 64 neighbours
+        } else {
+            T = 0u;   // warp-uniform (one node per warp): fall back to bitmap windows
+        }
+        if (G == 32 && T == 0u && u >= 0) T = warp_mex_above64(P, b, e, bm);
+        if (sub == 0 && u >= 0) {
+            P.X[u] = T;
+            if (STATS) my_edges[0] += e - b;
+        }
+    } else {
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) {
+            cnt += __shfl_xor_sync(FULL, cnt, o);
+            low += __shfl_xor_sync(FULL, low, o);
+        }
+        if (sub == 0 && u >= 0) {
+            my_conf += cnt;
+            if (STATS) my_edges[1] += low;
+            if (cnt) out[atomicAdd(out_cnt, 1u)] = u;
+            else P.X[u] = xu | FBIT;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ hub (CTA)
 template <typename OffT>
-__device__ unsigned assign_hub(const Params &P, const OffT *ro, int u, Smem &sm) {
+__device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm) {
     const long long b = ro[u], e = ro[u + 1];
     const unsigned lim = (unsigned)(e - b) + 1u;
     for (unsigned w0 = 0;; w0 += HUB_WORDS * 32) {
@@ -233,7 +297,7 @@ __device__ unsigned assign_hub(const Params &P, const OffT *ro, int u, Smem &sm)
         for (long long k = b + threadIdx.x; k < e; k += 4 * BLOCK) {
             int v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? P.ci[k + q * BLOCK] : -1;
+            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? ld_col(P.ci + k + q * BLOCK) : -1;
             unsigned x[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? P.X[v[q]] : 0u;
@@ -258,7 +322,7 @@ __device__ unsigned assign_hub(const Params &P, const OffT *ro, int u, Smem &sm)
 }
 
 template <typename OffT>
-__device__ unsigned resolve_hub(const Params &P, const OffT *ro, int u, unsigned T, Smem &sm,
+__device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned T, Smem &sm,
                                 unsigned &lower_out) {
     const long long b = ro[u], e = ro[u + 1];
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
@@ -270,7 +334,7 @@ __device__ unsigned resolve_hub(const Params &P, const OffT *ro, int u, unsigned
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long k = k0 + 32 * q + lane;
-            v[q] = k < e ? P.ci[k] : 0x7fffffff;
+            v[q] = k < e ? ld_col(P.ci + k) : 0x7fffffff;
         }
         unsigned x[4];
 #pragma unroll
@@ -294,16 +358,15 @@ __device__ unsigned resolve_hub(const Params &P, const OffT *ro, int u, unsigned
     return (unsigned)r;
 }
 
-// ------------------------------------------------------------------ small
+// ------------------------------------------------------------------ bin 0
 // Thread per node, NPT nodes per thread; all list / offset / first-four-
 // neighbour loads of the NPT nodes are issued before any is consumed.
-// Returns the loser flags (resolve) through `lost`.
 template <typename OffT, bool STATS, int PHASE>
 __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
                                            unsigned long long hi, int u[NPT], bool lost[NPT],
                                            unsigned long long &my_conf, unsigned long long *my_edges) {
-    const List &L = rc.L[BIN_SMALL];
+    const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
     unsigned xu[NPT];
 #pragma unroll
@@ -332,7 +395,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
     for (int j = 0; j < NPT; ++j)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) nb[j][q] = rb[j] + q < re[j] ? P.ci[rb[j] + q] : -1;
+        for (int q = 0; q < 4; ++q) nb[j][q] = rb[j] + q < re[j] ? ld_col(P.ci + rb[j] + q) : -1;
     if (PHASE == 0) {
         unsigned x[NPT][4];
 #pragma unroll
@@ -344,22 +407,16 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
             if (u[j] < 0) continue;
             unsigned long long mask = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const unsigned cc = x[j][q] & CMASK;
-                if ((x[j][q] & FBIT) && cc <= 64u) mask |= 1ull << (cc - 1u);
-            }
+            for (int q = 0; q < 4; ++q) mask_add(mask, x[j][q]);
             for (OffT k = rb[j] + 4; k < re[j]; k += 4) {  // deg 5..16
                 int v2[4];
                 unsigned x2[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? P.ci[k + q] : -1;
+                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? ld_col(P.ci + k + q) : -1;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) x2[q] = v2[q] >= 0 ? P.X[v2[q]] : 0u;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const unsigned cc = x2[q] & CMASK;
-                    if ((x2[q] & FBIT) && cc <= 64u) mask |= 1ull << (cc - 1u);
-                }
+                for (int q = 0; q < 4; ++q) mask_add(mask, x2[q]);
             }
             P.X[u[j]] = (unsigned)__ffsll((long long)~mask);  // deg <= 16: a zero bit exists
             if (STATS) my_edges[0] += re[j] - rb[j];
@@ -385,7 +442,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
                 int v2[4];
                 unsigned x2[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? P.ci[k + q] : 0x7fffffff;
+                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? ld_col(P.ci + k + q) : 0x7fffffff;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) x2[q] = v2[q] < u[j] ? P.X[v2[q]] : 0u;
 #pragma unroll
@@ -437,39 +494,59 @@ __device__ __forceinline__ unsigned compact_tile(const int u[NPT], const bool lo
     return tot;
 }
 
+// a chunk of a group bin: warps take warp tiles of 32/G nodes round-robin
+template <int G, typename OffT, bool STATS, int PHASE>
+__device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Smem &sm, int bin,
+                                            unsigned c, int np, unsigned long long &my_conf,
+                                            unsigned long long *my_edges) {
+    const RoundCfg &rc = sm.rc;
+    const unsigned warp = threadIdx.x >> 5;
+    const unsigned csz = rc.csz[bin];
+    const unsigned long long lo = (unsigned long long)c * csz;
+    const unsigned long long hi = min(lo + csz, rc.L[bin].total);
+    int *out = P.dyn[np][bin] + (long long)c * csz;
+    if (threadIdx.x == 0) sm.out_cnt = 0;
+    __syncthreads();
+    constexpr unsigned NG = 32 / G;
+    for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG)
+        group_tile<G, OffT, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out,
+                                          &sm.out_cnt, sm.win_bm[warp], my_conf, my_edges);
+    __syncthreads();
+    if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][bin][c] = sm.out_cnt;
+}
+
 // One unit of one phase.  All CTA-uniform inputs come from shared memory.
+// Unit ranges: [ubase0, ubase1) hubs, then bins 3, 2, 1, 0.
 template <typename OffT, bool STATS, int PHASE>
 __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &sm, unsigned unit,
                                          int p, unsigned long long &my_conf,
                                          unsigned long long *my_edges) {
     const RoundCfg &rc = sm.rc;
     const int np = p ^ 1;
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    const unsigned n_hub = rc.n_hub, nch1 = rc.nch1;
-    const bool cta_unit = unit < n_hub || (rc.mid_by_cta && unit < n_hub + nch1);
-    if (cta_unit) {
-        // ---- hub (or mid node in the latency regime): one CTA per node
-        const bool is_hub = unit < n_hub;
-        const unsigned c = unit - n_hub;
-        const int u = is_hub ? rc.L[BIN_HUB].base[unit] : rc.L[BIN_MID].base[list_index(rc.L[BIN_MID], sm.prefix[1], c)];
+    const unsigned *ub = rc.ubase;
+    const bool is_hub = unit < ub[1];
+    if (is_hub || (rc.bin3_by_cta && unit < ub[2])) {
+        // ---- hub (or bin-3 node in the latency regime): one CTA per node
+        const unsigned c = is_hub ? unit : unit - ub[1];
+        const int u = is_hub ? rc.L[BIN_HUB].base[c] : rc.L[3].base[list_index(rc.L[3], sm.prefix[3], c)];
         const unsigned xu = P.X[u];
         unsigned pushed = 0;
         if (!(rc.topo && (xu & FBIT))) {  // topology sweep: inactive (_kernels.pyx:76)
             if (PHASE == 0) {
-                const unsigned T = assign_hub(P, ro, u, sm);
+                const unsigned T = assign_cta(P, ro, u, sm);
                 if (threadIdx.x == 0) {
                     P.X[u] = T;
                     if (STATS) my_edges[0] += ro[u + 1] - ro[u];
                 }
             } else {
                 unsigned low;
-                const unsigned k = resolve_hub(P, ro, u, xu, sm, low);
+                const unsigned k = resolve_cta(P, ro, u, xu, sm, low);
                 if (threadIdx.x == 0) {
                     my_conf += k;
                     if (STATS) my_edges[1] += low;
                     if (k) {
                         if (is_hub) P.dyn[np][BIN_HUB][atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
-                        else P.dyn[np][BIN_MID][c] = u;  // segment c, capacity 1
+                        else P.dyn[np][3][c] = u;  // segment c, capacity 1
                         pushed = 1;
                     } else {
                         P.X[u] = xu | FBIT;
@@ -477,47 +554,20 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
                 }
             }
         }
-        if (!is_hub && PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][1][c] = pushed;
-    } else if (unit < n_hub + nch1) {
-        // ---- mid chunk: one warp per node
-        const unsigned c = unit - n_hub;
-        const unsigned csz1 = rc.csz1;
-        const unsigned long long lo = (unsigned long long)c * csz1;
-        const unsigned long long hi = min(lo + csz1, rc.L[BIN_MID].total);
-        int *out = P.dyn[np][BIN_MID] + (long long)c * csz1;
-        if (threadIdx.x == 0) sm.out_cnt = 0;
-        __syncthreads();
-        for (unsigned long long v = lo + warp; v < hi; v += NW) {
-            const int u = rc.L[BIN_MID].base[list_index(rc.L[BIN_MID], sm.prefix[1], v)];
-            const unsigned xu = P.X[u];
-            if (rc.topo && (xu & FBIT)) continue;
-            if (PHASE == 0) {
-                unsigned deg;
-                const unsigned T = assign_mid(P, ro, u, sm.mid_bm[warp], deg);
-                if (lane == 0) {
-                    P.X[u] = T;
-                    if (STATS) my_edges[0] += deg;
-                }
-            } else {
-                unsigned low;
-                const unsigned k = resolve_mid(P, ro, u, xu, low);
-                if (lane == 0) {
-                    my_conf += k;
-                    if (STATS) my_edges[1] += low;
-                    if (k) out[atomicAdd(&sm.out_cnt, 1u)] = u;
-                    else P.X[u] = xu | FBIT;
-                }
-            }
-        }
-        __syncthreads();
-        if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][1][c] = sm.out_cnt;
+        if (!is_hub && PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][3][c] = pushed;
+    } else if (unit < ub[2]) {
+        group_chunk<32, OffT, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
+    } else if (unit < ub[3]) {
+        group_chunk<16, OffT, STATS, PHASE>(P, ro, sm, 2, unit - ub[2], np, my_conf, my_edges);
+    } else if (unit < ub[4]) {
+        group_chunk<8, OffT, STATS, PHASE>(P, ro, sm, 1, unit - ub[3], np, my_conf, my_edges);
     } else {
-        // ---- small chunk
-        const unsigned c = unit - n_hub - nch1;
-        const unsigned csz0 = rc.csz0;
+        // ---- bin 0 chunk
+        const unsigned c = unit - ub[4];
+        const unsigned csz0 = rc.csz[0];
         const unsigned long long lo = (unsigned long long)c * csz0;
-        const unsigned long long hi = min(lo + csz0, rc.L[BIN_SMALL].total);
-        int *out = P.dyn[np][BIN_SMALL] + (long long)c * csz0;
+        const unsigned long long hi = min(lo + csz0, rc.L[0].total);
+        int *out = P.dyn[np][0] + (long long)c * csz0;
         unsigned written = 0;
         for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
             int u[NPT];
@@ -537,7 +587,7 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem 
     __syncthreads();
     unsigned unit = sm.unit;
     __syncthreads();
-    while (unit < sm.rc.units) {
+    while (unit < sm.rc.ubase[NBIN]) {
         if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);  // prefetch the next unit
         run_unit<OffT, STATS, PHASE>(P, ro, sm, unit, p, my_conf, my_edges);
         __syncthreads();
@@ -560,12 +610,14 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
 
     for (long long u = gtid; u < P.n; u += gthreads) P.X[u] = 0u;
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBIN; ++b) rc.nst[b] = C->nstat[b];
-        rc.stat_lists[0] = P.stat;
-        rc.stat_lists[1] = P.stat + rc.nst[0];
-        rc.stat_lists[2] = P.stat + rc.nst[0] + rc.nst[1];
-        rc.ident_small = rc.nst[0] == (unsigned long long)P.n;  // all nodes small: sweep ids
-        rc.prev_nseg[0] = rc.prev_nseg[1] = rc.prev_cap[0] = rc.prev_cap[1] = 0;
+        unsigned long long off = 0;
+        for (int b = 0; b < NBIN; ++b) {
+            rc.nst[b] = C->nstat[b];
+            rc.stat_lists[b] = P.stat + off;
+            off += rc.nst[b];
+        }
+        rc.ident_small = rc.nst[0] == (unsigned long long)P.n;  // all nodes in bin 0: sweep ids
+        for (int b = 0; b < NSEG_BINS; ++b) rc.prev_nseg[b] = rc.prev_cap[b] = 0;
     }
     grid_sync(&C->bar, P.nblocks);
 
@@ -581,8 +633,12 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
         //      previous round's output (round 1: the full static lists)
         if (t > 1) {
 #pragma unroll 1
-            for (int b = 0; b < 2; ++b) {
+            for (int b = 0; b < NSEG_BINS; ++b) {
                 const unsigned ns = rc.prev_nseg[b];
+                if (ns == 0) {  // CTA-uniform
+                    if (threadIdx.x == 0) sm.prefix[b][0] = 0;
+                    continue;
+                }
                 for (unsigned s = threadIdx.x; s < ns; s += BLOCK)
                     sm.prefix[b][s + 1] = __ldcg(&C->segcnt[p][b][s]);
                 if (threadIdx.x == 0) sm.prefix[b][0] = 0;
@@ -607,27 +663,35 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
             }
         }
         if (threadIdx.x == 0) {
-            for (int b = 0; b < 2; ++b)
+            for (int b = 0; b < NSEG_BINS; ++b)
                 rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.nst[b], 0, 0, false}
                                  : List{P.dyn[p][b], sm.prefix[b][rc.prev_nseg[b]], rc.prev_nseg[b],
                                         rc.prev_cap[b], true};
             const unsigned long long hub_total = t == 1 ? rc.nst[BIN_HUB] : ld_relaxed_u64(&C->hub_cnt[p]);
             rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : P.dyn[p][BIN_HUB], hub_total, 0, 0, false};
-            const unsigned long long s = rc.L[0].total + rc.L[1].total + rc.L[2].total;
+            unsigned long long s = 0;
+            for (int b = 0; b < NBIN; ++b) s += rc.L[b].total;
             const bool topo = P.mode == HC_MODE_TOPO || (P.mode == HC_MODE_HYBRID && (long long)s > P.thr);
-            // mid nodes at CTA granularity when few are active (latency regime)
-            const bool mid_cta = rc.L[1].total <= 2ull * P.nblocks;
+            // bin-3 nodes at CTA granularity when few are active (latency regime)
+            const bool bin3_cta = rc.L[3].total <= 2ull * P.nblocks;
             if (topo)  // topology-driven: sweep the static lists, activity test
                 for (int b = 0; b < NBIN; ++b) rc.L[b] = List{rc.stat_lists[b], rc.nst[b], 0, 0, false};
             rc.topo = topo;
             rc.ident = topo && rc.ident_small;
-            rc.csz0 = chunk_size(rc.L[0].total, BLOCK * NPT);
-            rc.csz1 = (mid_cta && rc.L[1].total <= MAXSEG) ? 1u : chunk_size(rc.L[1].total, NW);
-            rc.nch0 = (unsigned)((rc.L[0].total + rc.csz0 - 1) / rc.csz0);
-            rc.nch1 = (unsigned)((rc.L[1].total + rc.csz1 - 1) / rc.csz1);
-            rc.mid_by_cta = rc.csz1 == 1u;
-            rc.n_hub = (unsigned)rc.L[BIN_HUB].total;
-            rc.units = s == 0 ? 0u : rc.n_hub + rc.nch1 + rc.nch0;
+            rc.csz[0] = chunk_size(rc.L[0].total, BLOCK * NPT);
+            rc.csz[1] = chunk_size(rc.L[1].total, NW * 4);
+            rc.csz[2] = chunk_size(rc.L[2].total, NW * 2);
+            rc.csz[3] = (bin3_cta && rc.L[3].total <= MAXSEG) ? 1u : chunk_size(rc.L[3].total, NW);
+            for (int b = 0; b < NSEG_BINS; ++b)
+                rc.nch[b] = (unsigned)((rc.L[b].total + rc.csz[b] - 1) / rc.csz[b]);
+            rc.bin3_by_cta = rc.csz[3] == 1u;
+            const bool live = s != 0;
+            rc.ubase[0] = 0;
+            rc.ubase[1] = live ? (unsigned)rc.L[BIN_HUB].total : 0u;
+            rc.ubase[2] = rc.ubase[1] + (live ? rc.nch[3] : 0u);
+            rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
+            rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
+            rc.ubase[5] = rc.ubase[4] + (live ? rc.nch[0] : 0u);
             sm.red = s;  // broadcast |W_t|
             if (blockIdx.x == 0) {
                 const unsigned long long now = globaltimer();
@@ -679,10 +743,11 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
                 }
             }
         }
-        if (threadIdx.x == 0) {
-            rc.prev_nseg[0] = rc.nch0; rc.prev_nseg[1] = rc.nch1;
-            rc.prev_cap[0] = rc.csz0; rc.prev_cap[1] = rc.csz1;
-        }
+        if (threadIdx.x == 0)
+            for (int b = 0; b < NSEG_BINS; ++b) {
+                rc.prev_nseg[b] = rc.nch[b];
+                rc.prev_cap[b] = rc.csz[b];
+            }
         grid_sync(&C->bar, P.nblocks);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -692,20 +757,39 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
     for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(P.X[u] & CMASK);
 }
 
-// degree classifier for the static bins
-struct DegreeBin {
+// degree bins for the static lists: the partition primitive handles up to 3
+// bins per pass, so bins 0-2 and 3-4 are split over two passes and joined
+struct BinLow {
     const long long *ro;
     __device__ int operator()(long long i) const {
-        const long long d = ro[i + 1] - ro[i];
-        return d <= SMALL_MAX ? BIN_SMALL : (d <= MID_MAX ? BIN_MID : BIN_HUB);
+        const int b = bin_of_degree(ro[i + 1] - ro[i]);
+        return b <= 2 ? b : -1;
+    }
+};
+struct BinHigh {
+    const long long *ro;
+    __device__ int operator()(long long i) const {
+        const int b = bin_of_degree(ro[i + 1] - ro[i]);
+        return b >= 3 ? b - 3 : -1;
     }
 };
 struct EmitI32 {
     __device__ int operator()(long long i) const { return (int)i; }
 };
 
-__global__ void copy_totals_kernel(const unsigned long long *totals, Ctrl *c) {
-    if (threadIdx.x < NBIN) c->nstat[threadIdx.x] = totals[threadIdx.x];
+__global__ void copy_totals_kernel(const unsigned long long *lo, const unsigned long long *hi, Ctrl *c) {
+    if (threadIdx.x < 3) c->nstat[threadIdx.x] = lo[threadIdx.x];
+    if (threadIdx.x < 2) c->nstat[3 + threadIdx.x] = hi[threadIdx.x];
+}
+
+// stat[size(bins 0-2) ...] = stat2[0 .. size(bins 3-4))
+__global__ void join_static_kernel(int *stat, const int *stat2, const unsigned long long *lo,
+                                   const unsigned long long *hi) {
+    const unsigned long long base = lo[0] + lo[1] + lo[2];
+    const unsigned long long cnt = hi[0] + hi[1];
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+         i += (unsigned long long)gridDim.x * blockDim.x)
+        stat[base + i] = stat2[i];
 }
 
 __global__ void narrow_offsets_kernel(const long long *ro, int *ro32, long long count) {
@@ -720,7 +804,7 @@ inline size_t seg_capacity(long long cnt) {
 }
 
 struct Layout {
-    size_t x, stat, dyn[2][NBIN], ro32, ctrl, part, total;
+    size_t x, stat, stat2, dyn[2][NBIN], ro32, ctrl, part, part2, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
@@ -730,6 +814,7 @@ static Layout layout(long long n) {
     size_t o = 0;
     L.x = o; o = align_up(o + 4 * (size_t)n, 256);
     L.stat = o; o = align_up(o + 4 * (size_t)n, 256);
+    L.stat2 = o; o = align_up(o + 4 * (size_t)n, 256);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) {
             L.dyn[p][b] = o;
@@ -737,7 +822,8 @@ static Layout layout(long long n) {
         }
     L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
     L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
-    L.part = o; o = align_up(o + part_scratch_bytes(NBIN, n), 256);
+    L.part = o; o = align_up(o + part_scratch_bytes(3, n), 256);
+    L.part2 = o; o = align_up(o + part_scratch_bytes(3, n), 256);
     L.total = o;
     return L;
 }
@@ -822,23 +908,27 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
         HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
 
     HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
-    unsigned long long *totals = nullptr;
     const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
-    int rc = ordered_partition<NBIN>(num_nodes, DegreeBin{ro64}, EmitI32{}, P.stat, ws + L.part,
-                                     &totals, st);
+    // static degree bins, order-preserving within each bin
+    unsigned long long *tot_lo = nullptr, *tot_hi = nullptr;
+    int *stat2 = reinterpret_cast<int *>(ws + L.stat2);
+    int rc = ordered_partition<3>(num_nodes, BinLow{ro64}, EmitI32{}, P.stat, ws + L.part, &tot_lo, st);
     if (rc != HC_OK) return rc;
-    copy_totals_kernel<<<1, 32, 0, st>>>(totals, P.ctrl);
+    rc = ordered_partition<2>(num_nodes, BinHigh{ro64}, EmitI32{}, stat2, ws + L.part2, &tot_hi, st);
+    if (rc != HC_OK) return rc;
+    const int sms = std::max(1, num_sms());
+    join_static_kernel<<<sms, 256, 0, st>>>(P.stat, stat2, tot_lo, tot_hi);
+    HC_CHECK_LAUNCH();
+    copy_totals_kernel<<<1, 32, 0, st>>>(tot_lo, tot_hi, P.ctrl);
     HC_CHECK_LAUNCH();
     if (narrow) {
-        const int sms = std::max(1, num_sms());
         narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro64, reinterpret_cast<int *>(ws + L.ro32),
                                                        num_nodes + 1);
         HC_CHECK_LAUNCH();
     }
 
     const int per_sm = occupancy();
-    const int sms = num_sms();
-    HC_REQUIRE(per_sm > 0 && sms > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
+    HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * sms);
     void *args[] = {&P};
     const void *fn = narrow ? (d_stats ? kernel_ptr<int, true>() : kernel_ptr<int, false>())
