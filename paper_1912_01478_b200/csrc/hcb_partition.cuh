@@ -130,3 +130,74 @@ int ordered_partition(long long count, Classify cls, Emit emit, OutT *out, void 
 }
 
 }  // namespace hcb
+
+namespace hcb {
+
+// ---------------------------------------------------------------------------
+// Bucket sort of an index range by a small key (K <= 32 buckets): per-tile
+// histograms, one-CTA scan (bucket-major), scatter through shared-memory
+// cursors.  Buckets come out in key order; within a bucket, tiles keep their
+// order (positions inside one tile follow shared-memory atomics).
+// ---------------------------------------------------------------------------
+template <int K, class Key>
+__global__ void __launch_bounds__(PART_THREADS) bucket_count_kernel(long long count, Key key,
+                                                                    unsigned long long *tile_counts,
+                                                                    long long tiles) {
+    __shared__ unsigned s_cnt[K];
+    for (int i = threadIdx.x; i < K; i += PART_THREADS) s_cnt[i] = 0;
+    __syncthreads();
+    const long long base = (long long)blockIdx.x * PART_TILE;
+    for (int j = 0; j < PART_ITEMS; ++j) {
+        const long long i = base + (long long)j * PART_THREADS + threadIdx.x;
+        if (i < count) {
+            const int b = key(i);
+            if (b >= 0) atomicAdd(&s_cnt[b], 1u);
+        }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < K; b += PART_THREADS)
+        tile_counts[(long long)b * tiles + blockIdx.x] = s_cnt[b];
+}
+
+template <int K, class Key, class Emit, class OutT>
+__global__ void __launch_bounds__(PART_THREADS) bucket_scatter_kernel(long long count, Key key, Emit emit,
+                                                                      const unsigned long long *tile_offsets,
+                                                                      long long tiles, OutT *out) {
+    __shared__ unsigned long long s_cur[K];
+    for (int b = threadIdx.x; b < K; b += PART_THREADS)
+        s_cur[b] = tile_offsets[(long long)b * tiles + blockIdx.x];
+    __syncthreads();
+    const long long base = (long long)blockIdx.x * PART_TILE;
+    for (int j = 0; j < PART_ITEMS; ++j) {
+        const long long i = base + (long long)j * PART_THREADS + threadIdx.x;
+        if (i < count) {
+            const int b = key(i);
+            if (b >= 0) out[atomicAdd(&s_cur[b], 1ull)] = emit(i);
+        }
+    }
+}
+
+template <int K, class Key, class Emit, class OutT>
+int bucket_sort(long long count, Key key, Emit emit, OutT *out, void *scratch,
+                unsigned long long **totals_out, cudaStream_t st) {
+    const long long tiles = part_tiles(count);
+    unsigned long long *tile_counts = reinterpret_cast<unsigned long long *>(scratch);
+    unsigned long long *totals = reinterpret_cast<unsigned long long *>(
+        reinterpret_cast<char *>(scratch) +
+        align_up(sizeof(unsigned long long) * (size_t)K * (size_t)tiles, 256));
+    if (totals_out) *totals_out = totals;
+    if (count == 0) {
+        HC_CUDA_TRY(cudaMemsetAsync(totals, 0, sizeof(unsigned long long) * K, st));
+        return HC_OK;
+    }
+    bucket_count_kernel<K><<<(unsigned)tiles, PART_THREADS, 0, st>>>(count, key, tile_counts, tiles);
+    HC_CHECK_LAUNCH();
+    part_scan_kernel<<<1, PART_SCAN_THREADS, 0, st>>>(tile_counts, (long long)K * tiles, K, tiles, totals);
+    HC_CHECK_LAUNCH();
+    bucket_scatter_kernel<K><<<(unsigned)tiles, PART_THREADS, 0, st>>>(count, key, emit, tile_counts,
+                                                                      tiles, out);
+    HC_CHECK_LAUNCH();
+    return HC_OK;
+}
+
+}  // namespace hcb

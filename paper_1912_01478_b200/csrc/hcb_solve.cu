@@ -757,39 +757,34 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
     for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(P.X[u] & CMASK);
 }
 
-// degree bins for the static lists: the partition primitive handles up to 3
-// bins per pass, so bins 0-2 and 3-4 are split over two passes and joined
-struct BinLow {
+// Static lists: nodes bucket-sorted by a degree key.  Keys 0-2 are bins 0-2;
+// bin 3 and the hubs are split into power-of-two degree buckets in
+// DESCENDING order, so chunks of those bins hold nodes of similar degree
+// (balanced warps) and the heaviest nodes are handed out first.
+constexpr int NKEY = 15;
+__host__ __device__ constexpr int key_bin(int key) {
+    return key <= 2 ? key : key <= 8 ? 3 : 4;
+}
+struct DegreeKey {
     const long long *ro;
     __device__ int operator()(long long i) const {
-        const int b = bin_of_degree(ro[i + 1] - ro[i]);
-        return b <= 2 ? b : -1;
-    }
-};
-struct BinHigh {
-    const long long *ro;
-    __device__ int operator()(long long i) const {
-        const int b = bin_of_degree(ro[i + 1] - ro[i]);
-        return b >= 3 ? b - 3 : -1;
+        const long long d = ro[i + 1] - ro[i];
+        const int b = bin_of_degree(d);
+        if (b <= 2) return b;
+        const int lg = 64 - __clzll(d - 1);  // ceil(log2 d): 65..128 -> 7, 2049..4096 -> 12
+        if (b == 3) return 3 + (12 - lg);    // keys 3..8
+        return 9 + max(0, 18 - lg);          // hubs: >= 2^17+1 -> 9 ... 4097..8192 -> 14
     }
 };
 struct EmitI32 {
     __device__ int operator()(long long i) const { return (int)i; }
 };
 
-__global__ void copy_totals_kernel(const unsigned long long *lo, const unsigned long long *hi, Ctrl *c) {
-    if (threadIdx.x < 3) c->nstat[threadIdx.x] = lo[threadIdx.x];
-    if (threadIdx.x < 2) c->nstat[3 + threadIdx.x] = hi[threadIdx.x];
-}
-
-// stat[size(bins 0-2) ...] = stat2[0 .. size(bins 3-4))
-__global__ void join_static_kernel(int *stat, const int *stat2, const unsigned long long *lo,
-                                   const unsigned long long *hi) {
-    const unsigned long long base = lo[0] + lo[1] + lo[2];
-    const unsigned long long cnt = hi[0] + hi[1];
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
-         i += (unsigned long long)gridDim.x * blockDim.x)
-        stat[base + i] = stat2[i];
+__global__ void copy_totals_kernel(const unsigned long long *tot, Ctrl *c) {
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NBIN; ++b) c->nstat[b] = 0;
+        for (int k = 0; k < NKEY; ++k) c->nstat[key_bin(k)] += tot[k];
+    }
 }
 
 __global__ void narrow_offsets_kernel(const long long *ro, int *ro32, long long count) {
@@ -804,7 +799,7 @@ inline size_t seg_capacity(long long cnt) {
 }
 
 struct Layout {
-    size_t x, stat, stat2, dyn[2][NBIN], ro32, ctrl, part, part2, total;
+    size_t x, stat, dyn[2][NBIN], ro32, ctrl, part, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
@@ -814,7 +809,6 @@ static Layout layout(long long n) {
     size_t o = 0;
     L.x = o; o = align_up(o + 4 * (size_t)n, 256);
     L.stat = o; o = align_up(o + 4 * (size_t)n, 256);
-    L.stat2 = o; o = align_up(o + 4 * (size_t)n, 256);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) {
             L.dyn[p][b] = o;
@@ -822,8 +816,7 @@ static Layout layout(long long n) {
         }
     L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
     L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
-    L.part = o; o = align_up(o + part_scratch_bytes(3, n), 256);
-    L.part2 = o; o = align_up(o + part_scratch_bytes(3, n), 256);
+    L.part = o; o = align_up(o + part_scratch_bytes(NKEY, n), 256);
     L.total = o;
     return L;
 }
@@ -909,17 +902,12 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
 
     HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
     const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
-    // static degree bins, order-preserving within each bin
-    unsigned long long *tot_lo = nullptr, *tot_hi = nullptr;
-    int *stat2 = reinterpret_cast<int *>(ws + L.stat2);
-    int rc = ordered_partition<3>(num_nodes, BinLow{ro64}, EmitI32{}, P.stat, ws + L.part, &tot_lo, st);
-    if (rc != HC_OK) return rc;
-    rc = ordered_partition<2>(num_nodes, BinHigh{ro64}, EmitI32{}, stat2, ws + L.part2, &tot_hi, st);
+    // static degree-bucketed lists (bins contiguous, see DegreeKey)
+    unsigned long long *totals = nullptr;
+    int rc = bucket_sort<NKEY>(num_nodes, DegreeKey{ro64}, EmitI32{}, P.stat, ws + L.part, &totals, st);
     if (rc != HC_OK) return rc;
     const int sms = std::max(1, num_sms());
-    join_static_kernel<<<sms, 256, 0, st>>>(P.stat, stat2, tot_lo, tot_hi);
-    HC_CHECK_LAUNCH();
-    copy_totals_kernel<<<1, 32, 0, st>>>(tot_lo, tot_hi, P.ctrl);
+    copy_totals_kernel<<<1, 32, 0, st>>>(totals, P.ctrl);
     HC_CHECK_LAUNCH();
     if (narrow) {
         narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro64, reinterpret_cast<int *>(ws + L.ro32),
