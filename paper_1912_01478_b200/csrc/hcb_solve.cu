@@ -154,6 +154,27 @@ __device__ __forceinline__ long long list_index(const List &L, const unsigned *p
     return (long long)lo * L.segcap + (long long)(v - prefix[lo]);
 }
 
+// segment-walk variant: `s` is a segment at or before the one holding v (a
+// hint carried across increasing v), advanced in place
+__device__ __forceinline__ long long list_index_walk(const List &L, const unsigned *prefix,
+                                                     unsigned long long v, unsigned &s) {
+    if (!L.segmented) return (long long)v;
+    while (prefix[s + 1] <= v) ++s;
+    return (long long)s * L.segcap + (long long)(v - prefix[s]);
+}
+
+// segment holding v (binary search; v < total)
+__device__ __forceinline__ unsigned list_segment(const List &L, const unsigned *prefix, unsigned long long v) {
+    if (!L.segmented) return 0;
+    unsigned lo = 0, hi = L.nseg;
+    while (hi - lo > 1) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (prefix[mid] <= v) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
 // chunk size so a bin produces at most MAXSEG segments; multiple of `tile`
 __device__ __forceinline__ unsigned chunk_size(unsigned long long total, unsigned tile) {
     unsigned long long c = (total + MAXSEG - 1) / MAXSEG;
@@ -221,13 +242,22 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     unsigned long long mask = 0;
     unsigned cnt = 0, low = 0;
     bool stop = u < 0;
+    // software pipeline: the column ids of iteration it+1 are in flight while
+    // the X gathers of iteration it are issued
+    const int pad = PHASE == 0 ? -1 : 0x7fffffff;
+    int nb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const long long k = b + sub + q * G;
+        nb[q] = (!stop && k < e) ? ld_col(P.ci + k) : pad;
+    }
     for (unsigned it = 0; it < iters; ++it) {
-        const long long kb = b + (long long)it * 4 * G + sub;
-        int nb[4];
+        int nx[4];
+        const long long kn = b + (long long)(it + 1) * 4 * G + sub;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const long long k = kb + q * G;
-            nb[q] = (!stop && k < e) ? ld_col(P.ci + k) : (PHASE == 0 ? -1 : 0x7fffffff);
+            const long long k = kn + q * G;
+            nx[q] = (!stop && k < e) ? ld_col(P.ci + k) : pad;
         }
         if (PHASE == 0) {
             unsigned x[4];
@@ -251,7 +281,13 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << (gi * G));
             if (bal & gmask) stop = true;
             if (__all_sync(FULL, stop)) break;
+            if (stop) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) nx[q] = pad;
+            }
         }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) nb[q] = nx[q];
     }
     if (PHASE == 0) {
 #pragma unroll
@@ -369,10 +405,11 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
     const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
     unsigned xu[NPT];
+    unsigned seg = ident ? 0u : list_segment(L, prefix, base);  // same for the whole CTA (broadcast)
 #pragma unroll
     for (int j = 0; j < NPT; ++j) {
         const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
-        u[j] = v < hi ? (ident ? (int)v : L.base[list_index(L, prefix, v)]) : -1;
+        u[j] = v < hi ? (ident ? (int)v : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
         lost[j] = false;
         xu[j] = 0u;
     }
