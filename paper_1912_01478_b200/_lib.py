@@ -15,7 +15,8 @@ from pathlib import Path
 import torch
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libhcb.so"
+# HCB_LIB selects an alternative in-tree build (tuning experiments only)
+LIB_PATH = PKG / os.environ.get("HCB_LIB", "libhcb.so")
 
 HC_OK = 0
 HC_ERR_INVALID = -1

@@ -62,9 +62,19 @@
 namespace hcb {
 namespace solve {
 
-constexpr int BLOCK = 1024;
+#ifndef HC_BLOCK
+#define HC_BLOCK 1024
+#endif
+#ifndef HC_NPT
+#define HC_NPT 4
+#endif
+constexpr int BLOCK = HC_BLOCK;
+#ifndef HC_MINB
+#define HC_MINB (1024 / HC_BLOCK)
+#endif
+constexpr int MIN_CTAS = HC_MINB;        // resident CTAs per SM the register budget targets
 constexpr int NW = BLOCK / 32;
-constexpr int NPT = 4;                   // bin-0 nodes per thread per tile
+constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 constexpr int NSEG_BINS = 4;             // bins 0..3 are segmented; bin 4 (hubs) is dense
 constexpr int BIN_HUB = 4;
 constexpr int NBIN = 5;
@@ -72,6 +82,7 @@ constexpr int HUB_MIN = 4097;            // deg >= HUB_MIN -> hub
 constexpr int HUB_WORDS = 512;           // CTA bitmap window: 16384 colors per pass
 constexpr int WIN_WORDS = 32;            // warp bitmap window: 1024 colors per pass
 constexpr int MAXSEG = 2048;             // output segments per bin per round
+static_assert(MAXSEG % BLOCK == 0, "prefix scan: whole items per thread");
 constexpr unsigned FBIT = 0x80000000u;
 constexpr unsigned CMASK = 0x7fffffffu;
 
@@ -413,20 +424,22 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
         lost[j] = false;
         xu[j] = 0u;
     }
+    // the row offsets are loaded together with the activity word (speculative
+    // for inactive nodes in topology sweeps): one dependent round trip less
+    OffT rb[NPT], re[NPT];
+#pragma unroll
+    for (int j = 0; j < NPT; ++j) {
+        rb[j] = u[j] >= 0 ? ro[u[j]] : OffT(0);
+        re[j] = u[j] >= 0 ? ro[u[j] + 1] : OffT(0);
+    }
     if (topo || PHASE == 1) {
 #pragma unroll
         for (int j = 0; j < NPT; ++j) xu[j] = u[j] >= 0 ? P.X[u[j]] : 0u;
         if (topo) {
 #pragma unroll
             for (int j = 0; j < NPT; ++j)
-                if (xu[j] & FBIT) u[j] = -1;  // inactive (_kernels.pyx:76-77, 135-136)
+                if (xu[j] & FBIT) { u[j] = -1; re[j] = rb[j]; }  // inactive (_kernels.pyx:76-77, 135-136)
         }
-    }
-    OffT rb[NPT], re[NPT];
-#pragma unroll
-    for (int j = 0; j < NPT; ++j) {
-        rb[j] = u[j] >= 0 ? ro[u[j]] : OffT(0);
-        re[j] = u[j] >= 0 ? ro[u[j] + 1] : OffT(0);
     }
     int nb[NPT][4];
 #pragma unroll
@@ -512,14 +525,23 @@ __device__ __forceinline__ unsigned compact_tile(const int u[NPT], const bool lo
         sm.warp_tmp[lane * NW + warp] = mine;
     }
     __syncthreads();
-    if (warp == 0) {  // scan NPT*NW = 128 counts, 4 per lane
-        unsigned a[4], sum = 0;
+    if (warp == 0) {  // scan the NPT*NW counts, CPL per lane
+        constexpr int CPL = (NPT * NW + 31) / 32;
+        unsigned a[CPL], sum = 0;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { a[q] = sm.warp_tmp[4 * lane + q]; sum += a[q]; }
+        for (int q = 0; q < CPL; ++q) {
+            const unsigned i = CPL * lane + q;
+            a[q] = i < NPT * NW ? sm.warp_tmp[i] : 0u;
+            sum += a[q];
+        }
         const unsigned incl = warp_incl_scan(sum);
         unsigned run = incl - sum;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) { sm.warp_tmp[4 * lane + q] = run; run += a[q]; }
+        for (int q = 0; q < CPL; ++q) {
+            const unsigned i = CPL * lane + q;
+            if (i < NPT * NW) sm.warp_tmp[i] = run;
+            run += a[q];
+        }
         if (lane == 31) sm.out_cnt = incl;
     }
     __syncthreads();
@@ -635,7 +657,7 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem 
 
 // ------------------------------------------------------------------ kernel
 template <typename OffT, bool STATS>
-__global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
+__global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
     __shared__ Smem sm;
     Ctrl *C = P.ctrl;
     const OffT *ro = reinterpret_cast<const OffT *>(P.ro);
@@ -680,22 +702,31 @@ __global__ void __launch_bounds__(BLOCK, 1) solve_kernel(Params P) {
                     sm.prefix[b][s + 1] = __ldcg(&C->segcnt[p][b][s]);
                 if (threadIdx.x == 0) sm.prefix[b][0] = 0;
                 __syncthreads();
-                // inclusive scan of prefix[1..ns] (ns <= MAXSEG = 2*BLOCK)
-                const unsigned i0 = 1 + 2 * threadIdx.x, i1 = i0 + 1;
-                const unsigned a0 = i0 <= ns ? sm.prefix[b][i0] : 0u;
-                const unsigned a1 = i1 <= ns ? sm.prefix[b][i1] : 0u;
-                const unsigned pair = a0 + a1;
-                const unsigned incl = warp_incl_scan(pair);
+                // inclusive scan of prefix[1..ns] (ns <= MAXSEG), PPT items per thread
+                constexpr int PPT = MAXSEG / BLOCK;
+                unsigned a[PPT], sum = 0;
+#pragma unroll
+                for (int q = 0; q < PPT; ++q) {
+                    const unsigned i = 1 + PPT * threadIdx.x + q;
+                    a[q] = i <= ns ? sm.prefix[b][i] : 0u;
+                    sum += a[q];
+                }
+                const unsigned incl = warp_incl_scan(sum);
                 if (lane == 31) sm.warp_tmp[warp] = incl;
                 __syncthreads();
                 if (warp == 0) {
-                    const unsigned v = sm.warp_tmp[lane];
-                    sm.warp_tmp[lane] = warp_incl_scan(v) - v;
+                    const unsigned v = lane < NW ? sm.warp_tmp[lane] : 0u;
+                    const unsigned vi = warp_incl_scan(v);
+                    if (lane < NW) sm.warp_tmp[lane] = vi - v;
                 }
                 __syncthreads();
-                const unsigned ex = sm.warp_tmp[warp] + incl - pair;
-                if (i0 <= ns) sm.prefix[b][i0] = ex + a0;
-                if (i1 <= ns) sm.prefix[b][i1] = ex + pair;
+                unsigned run = sm.warp_tmp[warp] + incl - sum;
+#pragma unroll
+                for (int q = 0; q < PPT; ++q) {
+                    const unsigned i = 1 + PPT * threadIdx.x + q;
+                    run += a[q];
+                    if (i <= ns) sm.prefix[b][i] = run;
+                }
                 __syncthreads();
             }
         }
