@@ -4,7 +4,7 @@
 // (pkg/src/hybridcolor/driver.py:122-176) together with the round functions
 // (coloring.py:113-176), the kernels (_kernels.pyx:29-149) and the worklist
 // swap (worklist.py:77-91) by ONE cooperatively launched persistent kernel
-// (one 1024-thread CTA per SM): every round is
+// (two 512-thread CTAs per SM): every round is
 //     assign -> grid barrier -> resolve -> grid barrier
 // with the hybrid mode decision, the worklist and the per-round records kept
 // on the device, so there is no host round trip per round.
@@ -63,7 +63,7 @@ namespace hcb {
 namespace solve {
 
 #ifndef HC_BLOCK
-#define HC_BLOCK 1024
+#define HC_BLOCK 512
 #endif
 #ifndef HC_NPT
 #define HC_NPT 4
