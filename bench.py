@@ -304,7 +304,7 @@ def run_ours(args, cfg):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stream = torch.cuda.current_stream()
-    launches_per_step = 5  # partition count/scan/write + copy_totals + solve_kernel
+    launches_per_step = 6  # bucket count/scan/scatter + copy_totals + narrow_offsets + solve_kernel
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
