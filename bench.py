@@ -259,6 +259,83 @@ def build_graph(hc, cfg):
     return hc.rmat_graph(cfg["scale"], cfg["edgefactor"], cfg["seed"])
 
 
+def run_distributed(args, cfg):
+    """N > 1: the 1D-partitioned solve (paper_1912_01478_b200.distributed) over
+    NCCL, one rank per GPU, the same graph on every rank (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1912_01478_b200 as hc
+    from paper_1912_01478_b200.distributed import dist_color_graph
+
+    world = int(os.environ["WORLD_SIZE"])
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    dg = build_graph(hc, cfg)
+    n, und = dg.num_nodes, dg.num_undirected_edges
+    hcfg = hc.HybridConfig(mode=args.mode)
+    ro_host = dg.row_offsets.cpu().numpy()
+    for _ in range(args.warmup):
+        dist_color_graph(dg.row_offsets, dg.col_indices, n, hcfg, host_row_offsets=ro_host)
+    stream = torch.cuda.current_stream()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    res = None
+    with Clocks(local) as clk:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            res = dist_color_graph(dg.row_offsets, dg.col_indices, n, hcfg, host_row_offsets=ro_host)
+            stops[i].record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    total_ms = float(sum(a.elapsed_time(b) for a, b in zip(starts, stops)))
+    t = torch.tensor([total_ms], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = und * args.steps / (total_ms / 1e3)
+    # e2e: host CSR (pinned) uploaded by every rank inside the timed region
+    host = hc.CsrGraph.pinned(dg.to_host())
+    e2e_total = 0.0
+    for i in range(args.warmup + args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        d2 = host.to_device(dev)
+        r2 = dist_color_graph(d2.row_offsets, d2.col_indices, n, hcfg, host_row_offsets=ro_host)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_total += (time.perf_counter() - t0) * 1e3
+        del d2
+    t = torch.tensor([e2e_total], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_total = float(t.item())
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPU",
+            "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": args.mode,
+                       "num_nodes": n, "num_undirected_edges": und, "rounds": res.report.total_rounds,
+                       "parallelism": f"1d-partition x{world} (edge-balanced), NCCL exchange of boundary "
+                                      f"updates per phase", "exchanged_pairs": res.exchanged_pairs,
+                       "l2": "inputs > L2 per rank not guaranteed; no flush between steps"},
+            "clocks": clk.summary(),
+            "gpu_launches": (4 * res.report.total_rounds + 3) * args.steps,
+            "e2e": {"value": und * args.steps / (e2e_total / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": world * (8 * (n + 1) + 8 * dg.num_edges),
+                    "d2h_bytes_per_step": world * 8 * n},
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0
+
+
 def run_ours(args, cfg):
     import ctypes
 
@@ -417,6 +494,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_distributed(args, cfg)
     return run_ours(args, cfg)
 
 

@@ -140,6 +140,27 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
                    void *d_ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* 1D-partitioned multi-GPU solve: per-phase kernels  */
+/* over the owned range [lo, hi) with a replicated state word X[n]      */
+/* (0 / T / C|0x80000000).  Collectives between phases are the caller's */
+/* (torch.distributed / NCCL).  Work items: d_list[0..count) or, when   */
+/* d_list is NULL, the topology sweep lo..lo+count-1 with the activity   */
+/* test.  Boundary flags are relative to lo (flags[u-lo]); only boundary */
+/* nodes emit exchange pairs.  Counters are device int64, accumulated.   */
+/* ------------------------------------------------------------------ */
+int hc_dist_boundary(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t lo, int64_t hi,
+                     uint8_t *d_flags, void *stream);
+int hc_dist_assign(const int64_t *d_row_offsets, const int32_t *d_col_indices, uint32_t *d_X,
+                   const int32_t *d_list, int64_t count, int64_t lo, const uint8_t *d_boundary,
+                   int32_t *d_out_ids, uint32_t *d_out_vals, int64_t *d_out_cnt, void *stream);
+int hc_dist_resolve(const int64_t *d_row_offsets, const int32_t *d_col_indices, uint32_t *d_X,
+                    const int32_t *d_list, int64_t count, int64_t lo, const uint8_t *d_boundary,
+                    int32_t *d_next, int64_t *d_next_cnt, int32_t *d_out_ids, uint32_t *d_out_vals,
+                    int64_t *d_out_cnt, int64_t *d_conflicts, void *stream);
+int hc_dist_apply(uint32_t *d_X, const int32_t *d_ids, const uint32_t *d_vals, int64_t count, void *stream);
+int hc_dist_colors(const uint32_t *d_X, int64_t lo, int64_t hi, int64_t *d_colors, void *stream);
+
+/* ------------------------------------------------------------------ */
 /* Graph construction / generators / verification.                      */
 /* ------------------------------------------------------------------ */
 
