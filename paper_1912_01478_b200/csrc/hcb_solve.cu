@@ -56,6 +56,7 @@
 // preprocessing), halving the offset traffic; int64 otherwise.  Column loads
 // are streaming (evict-first) so the X gathers keep L2.
 #include <algorithm>
+#include <type_traits>
 
 #include "hcb_partition.cuh"
 
@@ -118,6 +119,7 @@ struct Params {
     long long thr;
     unsigned nblocks;
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
+    long long m;               // number of column ids
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -141,8 +143,65 @@ struct RoundCfg {
     bool topo, ident, bin3_by_cta, ident_small;
 };
 
+// ------------------------------------------------------------------ staging
+// Contiguous tiles (topology sweeps of bin 0 when every node is in bin 0:
+// grids, road networks) are staged into shared memory with the bulk-async
+// copy engine (cp.async.bulk + mbarrier, double buffered): the tile's state
+// words, row offsets and its whole column span arrive in three bulk copies,
+// so only the neighbour gathers stay on the critical path.
+constexpr int ST_NODES = 1024;                 // nodes per staged tile
+constexpr int ST_NPT = ST_NODES / BLOCK;       // nodes per thread
+constexpr int ST_CI = 6144;                    // staged column ids per tile (else direct loads)
+constexpr int ST_STAGES = 2;
+
+struct Stage {
+    unsigned X[ST_NODES];
+    int ro[ST_NODES + 8];
+    int ci[ST_CI];
+};
+constexpr size_t STAGE_SMEM = sizeof(Stage) * ST_STAGES;
+
+struct StageCtl {
+    unsigned long long bar_a[ST_STAGES];       // X + row offsets landed
+    unsigned long long bar_b[ST_STAGES];       // column span landed (or skipped)
+    int lo16[ST_STAGES];                       // first staged column index
+    int ci_ok[ST_STAGES];                      // column span staged?
+    unsigned count;                            // staged tiles consumed by this CTA
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "HC_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra HC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 struct Smem {
     RoundCfg rc;
+    StageCtl stc;
     unsigned prefix[NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
     unsigned win_bm[NW][WIN_WORDS];
     unsigned hub_bm[HUB_WORDS];
@@ -510,28 +569,31 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
 }
 
 // Ordered compaction of a tile's losers (index order base + j*BLOCK + tid,
-// i.e. j-major then thread) into out[written ...]; returns the tile's count.
-__device__ __forceinline__ unsigned compact_tile(const int u[NPT], const bool lost[NPT], int *out,
-                                                 unsigned written, Smem &sm) {
+// i.e. j-major then thread, K nodes per thread) into out[written ...];
+// returns the tile's count.
+template <int K>
+__device__ __forceinline__ unsigned compact_tile(const int *u, const bool *lost, int *out, unsigned written,
+                                                 Smem &sm) {
+    static_assert(K * NW <= NPT * NW || K <= NPT, "warp_tmp sized for NPT*NW counts");
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    unsigned bal[NPT];
+    unsigned bal[K];
 #pragma unroll
-    for (int j = 0; j < NPT; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
-    if (lane < NPT) {
+    for (int j = 0; j < K; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
+    if (lane < (unsigned)K) {
         unsigned mine = 0;
 #pragma unroll
-        for (int j = 0; j < NPT; ++j)
+        for (int j = 0; j < K; ++j)
             if (lane == (unsigned)j) mine = __popc(bal[j]);
         sm.warp_tmp[lane * NW + warp] = mine;
     }
     __syncthreads();
-    if (warp == 0) {  // scan the NPT*NW counts, CPL per lane
-        constexpr int CPL = (NPT * NW + 31) / 32;
+    if (warp == 0) {  // scan the K*NW counts, CPL per lane
+        constexpr int CPL = (K * NW + 31) / 32;
         unsigned a[CPL], sum = 0;
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
             const unsigned i = CPL * lane + q;
-            a[q] = i < NPT * NW ? sm.warp_tmp[i] : 0u;
+            a[q] = i < K * NW ? sm.warp_tmp[i] : 0u;
             sum += a[q];
         }
         const unsigned incl = warp_incl_scan(sum);
@@ -539,18 +601,149 @@ __device__ __forceinline__ unsigned compact_tile(const int u[NPT], const bool lo
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
             const unsigned i = CPL * lane + q;
-            if (i < NPT * NW) sm.warp_tmp[i] = run;
+            if (i < K * NW) sm.warp_tmp[i] = run;
             run += a[q];
         }
         if (lane == 31) sm.out_cnt = incl;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < NPT; ++j)
+    for (int j = 0; j < K; ++j)
         if (lost[j]) out[written + sm.warp_tmp[j * NW + warp] + __popc(bal[j] & lanemask_lt())] = u[j];
     const unsigned tot = sm.out_cnt;
     __syncthreads();
     return tot;
+}
+
+// ------------------------------------------------------------------ staged bin-0 sweep
+// producer side (one thread): stage the X words + row offsets of tile
+// [a, a+cnt), then (once they landed) its column span
+__device__ __forceinline__ void stage_issue_a(const Params &P, const int *ro, Stage &st, StageCtl &c, int s,
+                                              long long a, unsigned cnt) {
+    const unsigned bx = (cnt * 4u + 15u) & ~15u;
+    const unsigned br = ((cnt + 1u) * 4u + 15u) & ~15u;
+    mbar_expect_tx(&c.bar_a[s], bx + br);
+    bulk_g2s(st.X, P.X + a, bx, &c.bar_a[s]);
+    bulk_g2s(st.ro, ro + a, br, &c.bar_a[s]);
+}
+
+__device__ __forceinline__ void stage_issue_b(const Params &P, Stage &st, StageCtl &c, int s, unsigned cnt,
+                                              unsigned parity, long long m) {
+    mbar_wait(&c.bar_a[s], parity);
+    const int lo = st.ro[0], hi = st.ro[cnt];
+    const int lo16 = lo & ~3;
+    const long long hi16 = ((long long)hi + 3) & ~3LL;
+    c.lo16[s] = lo16;
+    if (hi16 - lo16 <= ST_CI && hi16 <= m && hi > lo) {
+        c.ci_ok[s] = 1;
+        const unsigned bytes = (unsigned)(hi16 - lo16) * 4u;
+        mbar_expect_tx(&c.bar_b[s], bytes);
+        bulk_g2s(st.ci, P.ci + lo16, bytes, &c.bar_b[s]);
+    } else {
+        c.ci_ok[s] = 0;  // span too large (or at the array end): direct loads
+        mbar_arrive(&c.bar_b[s]);
+    }
+}
+
+template <bool STATS, int PHASE>
+__device__ __forceinline__ void staged_tile(const Params &P, const Stage &st, const StageCtl &c, int s,
+                                            long long a, unsigned cnt, int u[ST_NPT], bool lost[ST_NPT],
+                                            unsigned long long &my_conf, unsigned long long *my_edges) {
+    const bool ci_ok = c.ci_ok[s];
+    const int lo16 = c.lo16[s];
+#pragma unroll
+    for (int j = 0; j < ST_NPT; ++j) {
+        const unsigned idx = j * BLOCK + threadIdx.x;
+        lost[j] = false;
+        u[j] = -1;
+        if (idx >= cnt) continue;
+        const unsigned xu = st.X[idx];
+        if (xu & FBIT) continue;  // topology sweep: inactive (_kernels.pyx:76-77, 135-136)
+        u[j] = (int)(a + idx);
+        const int rb = st.ro[idx], re = st.ro[idx + 1];
+        if (PHASE == 0) {
+            unsigned long long mask = 0;
+            for (int k0 = rb; k0 < re; k0 += 4) {
+                int nb[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    nb[q] = k0 + q < re ? (ci_ok ? st.ci[k0 + q - lo16] : ld_col(P.ci + k0 + q)) : -1;
+                unsigned x[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long long r = (long long)nb[q] - a;
+                    x[q] = nb[q] < 0 ? 0u : ((unsigned long long)r < cnt ? st.X[r] : P.X[nb[q]]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) mask_add(mask, x[q]);
+            }
+            P.X[u[j]] = (unsigned)__ffsll((long long)~mask);  // deg <= 16: a zero bit exists
+            if (STATS) my_edges[0] += re - rb;
+        } else {
+            unsigned cnt_k = 0, low = 0;
+            bool stop = false;
+            for (int k0 = rb; !stop && k0 < re; k0 += 4) {
+                int nb[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    nb[q] = k0 + q < re ? (ci_ok ? st.ci[k0 + q - lo16] : ld_col(P.ci + k0 + q)) : 0x7fffffff;
+                unsigned x[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const long long r = (long long)nb[q] - a;
+                    x[q] = nb[q] >= u[j] ? 0u : ((unsigned long long)r < cnt ? st.X[r] : P.X[nb[q]]);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (nb[q] < u[j]) { cnt_k += (x[q] & CMASK) == xu; ++low; }
+                    else stop = true;  // adjacency sorted ascending (graph.py:193-197)
+                }
+            }
+            my_conf += cnt_k;
+            if (STATS) my_edges[1] += low;
+            lost[j] = cnt_k != 0;
+            if (!lost[j]) P.X[u[j]] = xu | FBIT;
+        }
+    }
+}
+
+// a topology-ident bin-0 chunk [lo, hi) through the staged pipeline
+template <bool STATS, int PHASE>
+__device__ void staged_chunk(const Params &P, const int *ro, Smem &sm, Stage *stages, unsigned long long lo,
+                             unsigned long long hi, int *out, unsigned &written,
+                             unsigned long long &my_conf, unsigned long long *my_edges) {
+    StageCtl &c = sm.stc;
+    const unsigned ntiles = (unsigned)((hi - lo + ST_NODES - 1) / ST_NODES);
+    const unsigned g0 = c.count;  // CTA-uniform (read after the unit barrier)
+    auto tile_cnt = [&](unsigned i) { return (unsigned)min((unsigned long long)ST_NODES, hi - (lo + (unsigned long long)i * ST_NODES)); };
+    if (threadIdx.x == 0) {
+        for (unsigned i = 0; i < ntiles && i < ST_STAGES; ++i) {
+            const unsigned g = g0 + i;
+            stage_issue_a(P, ro, stages[g % ST_STAGES], c, g % ST_STAGES, (long long)(lo + (unsigned long long)i * ST_NODES), tile_cnt(i));
+        }
+        stage_issue_b(P, stages[g0 % ST_STAGES], c, g0 % ST_STAGES, tile_cnt(0), (g0 / ST_STAGES) & 1u, P.m);
+    }
+    for (unsigned i = 0; i < ntiles; ++i) {
+        const unsigned g = g0 + i, sidx = g % ST_STAGES, parity = (g / ST_STAGES) & 1u;
+        if (threadIdx.x == 0 && i + 1 < ntiles) {
+            const unsigned g1 = g + 1;
+            stage_issue_b(P, stages[g1 % ST_STAGES], c, g1 % ST_STAGES, tile_cnt(i + 1), (g1 / ST_STAGES) & 1u, P.m);
+        }
+        mbar_wait(&c.bar_a[sidx], parity);
+        mbar_wait(&c.bar_b[sidx], parity);
+        const long long a = (long long)(lo + (unsigned long long)i * ST_NODES);
+        const unsigned cnt = tile_cnt(i);
+        int u[ST_NPT];
+        bool lost[ST_NPT];
+        staged_tile<STATS, PHASE>(P, stages[sidx], c, sidx, a, cnt, u, lost, my_conf, my_edges);
+        if (PHASE == 1) written += compact_tile<ST_NPT>(u, lost, out, written, sm);
+        else __syncthreads();  // stage sidx fully consumed
+        if (threadIdx.x == 0 && i + ST_STAGES < ntiles) {
+            fence_proxy_async();  // generic reads of the stage before the async overwrite
+            stage_issue_a(P, ro, stages[sidx], c, sidx, a + (long long)ST_STAGES * ST_NODES, tile_cnt(i + ST_STAGES));
+        }
+    }
+    if (threadIdx.x == 0) c.count = g0 + ntiles;
 }
 
 // a chunk of a group bin: warps take warp tiles of 32/G nodes round-robin
@@ -628,11 +821,20 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         const unsigned long long hi = min(lo + csz0, rc.L[0].total);
         int *out = P.dyn[np][0] + (long long)c * csz0;
         unsigned written = 0;
+        if constexpr (std::is_same<OffT, int>::value) {
+            if (rc.ident) {  // contiguous tiles: bulk-async staged pipeline
+                extern __shared__ __align__(128) unsigned char dyn_smem[];
+                staged_chunk<STATS, PHASE>(P, ro, sm, reinterpret_cast<Stage *>(dyn_smem), lo, hi, out, written,
+                                           my_conf, my_edges);
+                if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
+                return;
+            }
+        }
         for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
             int u[NPT];
             bool lost[NPT];
             small_tile<OffT, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
-            if (PHASE == 1) written += compact_tile(u, lost, out, written, sm);
+            if (PHASE == 1) written += compact_tile<NPT>(u, lost, out, written, sm);
         }
         if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
     }
@@ -677,6 +879,12 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         }
         rc.ident_small = rc.nst[0] == (unsigned long long)P.n;  // all nodes in bin 0: sweep ids
         for (int b = 0; b < NSEG_BINS; ++b) rc.prev_nseg[b] = rc.prev_cap[b] = 0;
+        for (int st = 0; st < ST_STAGES; ++st) {
+            mbar_init(&sm.stc.bar_a[st], 1);
+            mbar_init(&sm.stc.bar_b[st], 1);
+        }
+        sm.stc.count = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     grid_sync(&C->bar, P.nblocks);
 
@@ -875,14 +1083,14 @@ struct Layout {
 static Layout layout(long long n) {
     Layout L;
     size_t o = 0;
-    L.x = o; o = align_up(o + 4 * (size_t)n, 256);
+    L.x = o; o = align_up(o + 4 * (size_t)n + 64, 256);  // +pad: 16-byte bulk copies of the tail tile
     L.stat = o; o = align_up(o + 4 * (size_t)n, 256);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) {
             L.dyn[p][b] = o;
             o = align_up(o + 4 * (b == BIN_HUB ? (size_t)n : seg_capacity(n)), 256);
         }
-    L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
+    L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1) + 64, 256);
     L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
     L.part = o; o = align_up(o + part_scratch_bytes(NKEY, n), 256);
     L.total = o;
@@ -894,9 +1102,23 @@ static const void *kernel_ptr() {
     return (const void *)solve_kernel<OffT, STATS>;
 }
 
+static bool configure_smem() {
+    static bool done = false;
+    if (!done) {
+        for (const void *fn : {kernel_ptr<int, false>(), kernel_ptr<int, true>()})
+            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STAGE_SMEM) !=
+                cudaSuccess)
+                return false;
+        done = true;
+    }
+    return true;
+}
+
 static int occupancy() {
     int per_sm = 0, per_sm64 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<int, false>, BLOCK, 0) != cudaSuccess)
+    if (!configure_smem()) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<int, false>, BLOCK, STAGE_SMEM) !=
+        cudaSuccess)
         return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm64, solve_kernel<long long, false>, BLOCK, 0) !=
         cudaSuccess)
@@ -965,6 +1187,7 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     P.mode = mode;
     P.thr = thr_count;
     P.stats = reinterpret_cast<long long *>(d_stats);
+    P.m = num_edges;
     if (d_stats && P.max_rec)
         HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
 
@@ -989,7 +1212,7 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     void *args[] = {&P};
     const void *fn = narrow ? (d_stats ? kernel_ptr<int, true>() : kernel_ptr<int, false>())
                             : (d_stats ? kernel_ptr<long long, true>() : kernel_ptr<long long, false>());
-    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
+    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, narrow ? STAGE_SMEM : 0, st));
     long long info[2];
     HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
