@@ -69,6 +69,9 @@ namespace solve {
 #ifndef HC_NPT
 #define HC_NPT 4
 #endif
+#ifndef HC_STAGE
+#define HC_STAGE 1
+#endif
 constexpr int BLOCK = HC_BLOCK;
 #ifndef HC_MINB
 #define HC_MINB (1024 / HC_BLOCK)
@@ -120,6 +123,7 @@ struct Params {
     unsigned nblocks;
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
     long long m;               // number of column ids
+    int staged;                // dynamic shared memory holds the staging buffers
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -149,9 +153,9 @@ struct RoundCfg {
 // copy engine (cp.async.bulk + mbarrier, double buffered): the tile's state
 // words, row offsets and its whole column span arrive in three bulk copies,
 // so only the neighbour gathers stay on the critical path.
-constexpr int ST_NODES = 1024;                 // nodes per staged tile
+constexpr int ST_NODES = BLOCK;                // nodes per staged tile (one per thread)
 constexpr int ST_NPT = ST_NODES / BLOCK;       // nodes per thread
-constexpr int ST_CI = 6144;                    // staged column ids per tile (else direct loads)
+constexpr int ST_CI = 2048;                    // staged column ids per tile (else direct loads)
 constexpr int ST_STAGES = 2;
 
 struct Stage {
@@ -822,7 +826,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         int *out = P.dyn[np][0] + (long long)c * csz0;
         unsigned written = 0;
         if constexpr (std::is_same<OffT, int>::value) {
-            if (rc.ident) {  // contiguous tiles: bulk-async staged pipeline
+            if (rc.ident && P.staged) {  // contiguous tiles: bulk-async staged pipeline
                 extern __shared__ __align__(128) unsigned char dyn_smem[];
                 staged_chunk<STATS, PHASE>(P, ro, sm, reinterpret_cast<Stage *>(dyn_smem), lo, hi, out, written,
                                            my_conf, my_edges);
@@ -1114,11 +1118,11 @@ static bool configure_smem() {
     return true;
 }
 
-static int occupancy() {
+static int occupancy(bool staged = false) {
     int per_sm = 0, per_sm64 = 0;
     if (!configure_smem()) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<int, false>, BLOCK, STAGE_SMEM) !=
-        cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<int, false>, BLOCK,
+                                                      staged ? STAGE_SMEM : 0) != cudaSuccess)
         return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm64, solve_kernel<long long, false>, BLOCK, 0) !=
         cudaSuccess)
@@ -1206,13 +1210,23 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
         HC_CHECK_LAUNCH();
     }
 
-    const int per_sm = occupancy();
+    // Staged sweeps need shared memory that would otherwise be L1: reserve it
+    // only when every node is in bin 0 (the sweeps can then stage tiles).
+    bool staged = false;
+    if (narrow && HC_STAGE) {
+        unsigned long long nst0 = 0;
+        HC_CUDA_TRY(cudaMemcpyAsync(&nst0, &P.ctrl->nstat[0], sizeof nst0, cudaMemcpyDeviceToHost, st));
+        HC_CUDA_TRY(cudaStreamSynchronize(st));
+        staged = nst0 == (unsigned long long)num_nodes;
+    }
+    P.staged = staged ? 1 : 0;
+    const int per_sm = occupancy(staged);
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * sms);
     void *args[] = {&P};
     const void *fn = narrow ? (d_stats ? kernel_ptr<int, true>() : kernel_ptr<int, false>())
                             : (d_stats ? kernel_ptr<long long, true>() : kernel_ptr<long long, false>());
-    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, narrow ? STAGE_SMEM : 0, st));
+    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, staged ? STAGE_SMEM : 0, st));
     long long info[2];
     HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
