@@ -56,7 +56,6 @@
 // preprocessing), halving the offset traffic; int64 otherwise.  Column loads
 // are streaming (evict-first) so the X gathers keep L2.
 #include <algorithm>
-#include <type_traits>
 
 #include "hcb_partition.cuh"
 
@@ -69,10 +68,10 @@ namespace solve {
 #ifndef HC_NPT
 #define HC_NPT 4
 #endif
-#ifndef HC_STAGE
-#define HC_STAGE 1
-#endif
 constexpr int BLOCK = HC_BLOCK;
+#ifndef HC_FMT16
+#define HC_FMT16 1
+#endif
 #ifndef HC_MINB
 #define HC_MINB (1024 / HC_BLOCK)
 #endif
@@ -110,8 +109,9 @@ struct Ctrl {
 struct Params {
     const void *ro;            // int32 or int64 row offsets (template OffT)
     const int *ci;
+    const short *ci16;         // delta-encoded columns (Fmt CT = short)
     long long n;
-    unsigned *X;
+    void *X;                   // state words (Fmt XT)
     int *stat;                 // static lists, bins contiguous
     int *dyn[2][NBIN];         // dynamic lists per parity and bin
     Ctrl *ctrl;
@@ -122,8 +122,6 @@ struct Params {
     long long thr;
     unsigned nblocks;
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
-    long long m;               // number of column ids
-    int staged;                // dynamic shared memory holds the staging buffers
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -147,65 +145,8 @@ struct RoundCfg {
     bool topo, ident, bin3_by_cta, ident_small;
 };
 
-// ------------------------------------------------------------------ staging
-// Contiguous tiles (topology sweeps of bin 0 when every node is in bin 0:
-// grids, road networks) are staged into shared memory with the bulk-async
-// copy engine (cp.async.bulk + mbarrier, double buffered): the tile's state
-// words, row offsets and its whole column span arrive in three bulk copies,
-// so only the neighbour gathers stay on the critical path.
-constexpr int ST_NODES = BLOCK;                // nodes per staged tile (one per thread)
-constexpr int ST_NPT = ST_NODES / BLOCK;       // nodes per thread
-constexpr int ST_CI = 2048;                    // staged column ids per tile (else direct loads)
-constexpr int ST_STAGES = 2;
-
-struct Stage {
-    unsigned X[ST_NODES];
-    int ro[ST_NODES + 8];
-    int ci[ST_CI];
-};
-constexpr size_t STAGE_SMEM = sizeof(Stage) * ST_STAGES;
-
-struct StageCtl {
-    unsigned long long bar_a[ST_STAGES];       // X + row offsets landed
-    unsigned long long bar_b[ST_STAGES];       // column span landed (or skipped)
-    int lo16[ST_STAGES];                       // first staged column index
-    int ci_ok[ST_STAGES];                      // column span staged?
-    unsigned count;                            // staged tiles consumed by this CTA
-};
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "HC_WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra HC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
 struct Smem {
     RoundCfg rc;
-    StageCtl stc;
     unsigned prefix[NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
     unsigned win_bm[NW][WIN_WORDS];
     unsigned hub_bm[HUB_WORDS];
@@ -260,8 +201,46 @@ __device__ __forceinline__ void mark(unsigned *bm, unsigned c) {
     atomicOr(&bm[(c - 1u) >> 5], 1u << ((c - 1u) & 31u));
 }
 
-// streaming load of a column id: evict-first so the X gathers keep L2
-__device__ __forceinline__ int ld_col(const int *p) { return __ldcs(p); }
+// Storage formats, chosen per graph by hc_solve:
+//   state word  XT = uint32 (bit 31 = committed)  or uint16 (bit 15), the
+//               latter when max degree <= 16384 so every color fits 15 bits
+//   column id   CT = int32 absolute  or int16 delta (v - u), the latter when
+//               every |v - u| < 2^15 (grids / meshes with local numbering)
+// All solver logic works on the 32-bit encoding; the accessors convert.
+template <typename XT, typename CT>
+struct Fmt {
+    using xt = XT;
+    using ct = CT;
+};
+using F32 = Fmt<unsigned, int>;
+using F16 = Fmt<unsigned short, int>;
+using F16D = Fmt<unsigned short, short>;
+using F32D = Fmt<unsigned, short>;
+
+template <class F>
+__device__ __forceinline__ unsigned xget(const Params &P, long long v) {
+    if constexpr (sizeof(typename F::xt) == 4) {
+        return reinterpret_cast<const unsigned *>(P.X)[v];
+    } else {
+        const unsigned s = reinterpret_cast<const unsigned short *>(P.X)[v];
+        return ((s & 0x8000u) << 16) | (s & 0x7fffu);
+    }
+}
+template <class F>
+__device__ __forceinline__ void xput(const Params &P, long long v, unsigned w) {
+    if constexpr (sizeof(typename F::xt) == 4)
+        reinterpret_cast<unsigned *>(P.X)[v] = w;
+    else
+        reinterpret_cast<unsigned short *>(P.X)[v] = (unsigned short)(((w >> 16) & 0x8000u) | (w & 0x7fffu));
+}
+// streaming load of a column id (evict-first so the X gathers keep L2)
+template <class F>
+__device__ __forceinline__ int colget(const Params &P, long long k, int u) {
+    if constexpr (sizeof(typename F::ct) == 4)
+        return __ldcs(P.ci + k);
+    else
+        return u + (int)__ldcs(P.ci16 + k);
+}
 
 __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
     const unsigned c = x & CMASK;
@@ -271,7 +250,8 @@ __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
 // ------------------------------------------------------------------ groups
 // Warp-level mex over window(s) above color 64, for a node whose colors
 // 1..64 are all taken (rare): whole warp, one node.
-__device__ unsigned warp_mex_above64(const Params &P, long long b, long long e, unsigned *bm) {
+template <class F>
+__device__ unsigned warp_mex_above64(const Params &P, int u, long long b, long long e, unsigned *bm) {
     const unsigned lane = lane_id();
     const unsigned lim = (unsigned)(e - b) + 1u;
     for (unsigned w0 = 64;; w0 += WIN_WORDS * 32) {
@@ -279,7 +259,7 @@ __device__ unsigned warp_mex_above64(const Params &P, long long b, long long e, 
         __syncwarp();
         const unsigned hi = min(lim, w0 + WIN_WORDS * 32);
         for (long long k = b + lane; k < e; k += 32) {
-            const unsigned x = P.X[ld_col(P.ci + k)];
+            const unsigned x = xget<F>(P, colget<F>(P, k, u));
             const unsigned c = x & CMASK;
             if ((x & FBIT) && c > w0 && c <= hi) mark(bm, c - w0);
         }
@@ -295,7 +275,7 @@ __device__ unsigned warp_mex_above64(const Params &P, long long b, long long e, 
 }
 
 // One warp tile of a group bin: 32/G nodes, G lanes per node.
-template <int G, typename OffT, bool STATS, int PHASE>
+template <int G, typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, const List &L,
                                            const unsigned *prefix, unsigned long long v0,
                                            unsigned long long hi, bool topo, int *out,
@@ -307,7 +287,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     int u = v < hi ? L.base[list_index(L, prefix, v)] : -1;
     unsigned xu = 0;
     if (topo || PHASE == 1) {
-        xu = u >= 0 ? P.X[u] : 0u;
+        xu = u >= 0 ? xget<F>(P, u) : 0u;
         if (topo && (xu & FBIT)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
     }
     const long long b = u >= 0 ? (long long)ro[u] : 0, e = u >= 0 ? (long long)ro[u + 1] : 0;
@@ -323,7 +303,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const long long k = b + sub + q * G;
-        nb[q] = (!stop && k < e) ? ld_col(P.ci + k) : pad;
+        nb[q] = (!stop && k < e) ? colget<F>(P, k, u) : pad;
     }
     for (unsigned it = 0; it < iters; ++it) {
         int nx[4];
@@ -331,18 +311,18 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long k = kn + q * G;
-            nx[q] = (!stop && k < e) ? ld_col(P.ci + k) : pad;
+            nx[q] = (!stop && k < e) ? colget<F>(P, k, u) : pad;
         }
         if (PHASE == 0) {
             unsigned x[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = nb[q] >= 0 ? P.X[nb[q]] : 0u;
+            for (int q = 0; q < 4; ++q) x[q] = nb[q] >= 0 ? xget<F>(P, nb[q]) : 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q) mask_add(mask, x[q]);
         } else {
             unsigned x[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = nb[q] < u ? P.X[nb[q]] : 0u;
+            for (int q = 0; q < 4; ++q) x[q] = nb[q] < u ? xget<F>(P, nb[q]) : 0u;
             bool ge = false;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -374,9 +354,9 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
         } else {
             T = 0u;   // warp-uniform (one node per warp): fall back to bitmap windows
         }
-        if (G == 32 && T == 0u && u >= 0) T = warp_mex_above64(P, b, e, bm);
+        if (G == 32 && T == 0u && u >= 0) T = warp_mex_above64<F>(P, u, b, e, bm);
         if (sub == 0 && u >= 0) {
-            P.X[u] = T;
+            xput<F>(P, u, T);
             if (STATS) my_edges[0] += e - b;
         }
     } else {
@@ -389,13 +369,13 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             my_conf += cnt;
             if (STATS) my_edges[1] += low;
             if (cnt) out[atomicAdd(out_cnt, 1u)] = u;
-            else P.X[u] = xu | FBIT;
+            else xput<F>(P, u, xu | FBIT);
         }
     }
 }
 
 // ------------------------------------------------------------------ hub (CTA)
-template <typename OffT>
+template <typename OffT, class F>
 __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm) {
     const long long b = ro[u], e = ro[u + 1];
     const unsigned lim = (unsigned)(e - b) + 1u;
@@ -407,10 +387,10 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
         for (long long k = b + threadIdx.x; k < e; k += 4 * BLOCK) {
             int v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? ld_col(P.ci + k + q * BLOCK) : -1;
+            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? colget<F>(P, k + q * BLOCK, u) : -1;
             unsigned x[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? P.X[v[q]] : 0u;
+            for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const unsigned c = x[q] & CMASK;
@@ -431,7 +411,7 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
     }
 }
 
-template <typename OffT>
+template <typename OffT, class F>
 __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned T, Smem &sm,
                                 unsigned &lower_out) {
     const long long b = ro[u], e = ro[u + 1];
@@ -444,11 +424,11 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long k = k0 + 32 * q + lane;
-            v[q] = k < e ? ld_col(P.ci + k) : 0x7fffffff;
+            v[q] = k < e ? colget<F>(P, k, u) : 0x7fffffff;
         }
         unsigned x[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[q] < u ? P.X[v[q]] : 0u;
+        for (int q = 0; q < 4; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
         bool stop = false;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -471,7 +451,7 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
 // ------------------------------------------------------------------ bin 0
 // Thread per node, NPT nodes per thread; all list / offset / first-four-
 // neighbour loads of the NPT nodes are issued before any is consumed.
-template <typename OffT, bool STATS, int PHASE>
+template <typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
                                            unsigned long long hi, int u[NPT], bool lost[NPT],
@@ -497,7 +477,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
     }
     if (topo || PHASE == 1) {
 #pragma unroll
-        for (int j = 0; j < NPT; ++j) xu[j] = u[j] >= 0 ? P.X[u[j]] : 0u;
+        for (int j = 0; j < NPT; ++j) xu[j] = u[j] >= 0 ? xget<F>(P, u[j]) : 0u;
         if (topo) {
 #pragma unroll
             for (int j = 0; j < NPT; ++j)
@@ -508,13 +488,13 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
     for (int j = 0; j < NPT; ++j)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) nb[j][q] = rb[j] + q < re[j] ? ld_col(P.ci + rb[j] + q) : -1;
+        for (int q = 0; q < 4; ++q) nb[j][q] = rb[j] + q < re[j] ? colget<F>(P, rb[j] + q, u[j]) : -1;
     if (PHASE == 0) {
         unsigned x[NPT][4];
 #pragma unroll
         for (int j = 0; j < NPT; ++j)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[j][q] = nb[j][q] >= 0 ? P.X[nb[j][q]] : 0u;
+            for (int q = 0; q < 4; ++q) x[j][q] = nb[j][q] >= 0 ? xget<F>(P, nb[j][q]) : 0u;
 #pragma unroll
         for (int j = 0; j < NPT; ++j) {
             if (u[j] < 0) continue;
@@ -525,13 +505,13 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
                 int v2[4];
                 unsigned x2[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? ld_col(P.ci + k + q) : -1;
+                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? colget<F>(P, k + q, u[j]) : -1;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) x2[q] = v2[q] >= 0 ? P.X[v2[q]] : 0u;
+                for (int q = 0; q < 4; ++q) x2[q] = v2[q] >= 0 ? xget<F>(P, v2[q]) : 0u;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) mask_add(mask, x2[q]);
             }
-            P.X[u[j]] = (unsigned)__ffsll((long long)~mask);  // deg <= 16: a zero bit exists
+            xput<F>(P, u[j], (unsigned)__ffsll((long long)~mask));  // deg <= 16: a zero bit exists
             if (STATS) my_edges[0] += re[j] - rb[j];
         }
     } else {
@@ -539,7 +519,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
         for (int j = 0; j < NPT; ++j)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[j][q] = (nb[j][q] >= 0 && nb[j][q] < u[j]) ? P.X[nb[j][q]] : 0u;
+            for (int q = 0; q < 4; ++q) x[j][q] = (nb[j][q] >= 0 && nb[j][q] < u[j]) ? xget<F>(P, nb[j][q]) : 0u;
 #pragma unroll
         for (int j = 0; j < NPT; ++j) {
             if (u[j] < 0) continue;
@@ -555,9 +535,9 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
                 int v2[4];
                 unsigned x2[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? ld_col(P.ci + k + q) : 0x7fffffff;
+                for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? colget<F>(P, k + q, u[j]) : 0x7fffffff;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) x2[q] = v2[q] < u[j] ? P.X[v2[q]] : 0u;
+                for (int q = 0; q < 4; ++q) x2[q] = v2[q] < u[j] ? xget<F>(P, v2[q]) : 0u;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     if (v2[q] < u[j]) { cnt += (x2[q] & CMASK) == T; ++low; }
@@ -567,37 +547,34 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
             my_conf += cnt;
             if (STATS) my_edges[1] += low;
             lost[j] = cnt != 0;
-            if (!lost[j]) P.X[u[j]] = T | FBIT;
+            if (!lost[j]) xput<F>(P, u[j], T | FBIT);
         }
     }
 }
 
 // Ordered compaction of a tile's losers (index order base + j*BLOCK + tid,
-// i.e. j-major then thread, K nodes per thread) into out[written ...];
-// returns the tile's count.
-template <int K>
-__device__ __forceinline__ unsigned compact_tile(const int *u, const bool *lost, int *out, unsigned written,
-                                                 Smem &sm) {
-    static_assert(K * NW <= NPT * NW || K <= NPT, "warp_tmp sized for NPT*NW counts");
+// i.e. j-major then thread) into out[written ...]; returns the tile's count.
+__device__ __forceinline__ unsigned compact_tile(const int u[NPT], const bool lost[NPT], int *out,
+                                                 unsigned written, Smem &sm) {
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    unsigned bal[K];
+    unsigned bal[NPT];
 #pragma unroll
-    for (int j = 0; j < K; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
-    if (lane < (unsigned)K) {
+    for (int j = 0; j < NPT; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
+    if (lane < NPT) {
         unsigned mine = 0;
 #pragma unroll
-        for (int j = 0; j < K; ++j)
+        for (int j = 0; j < NPT; ++j)
             if (lane == (unsigned)j) mine = __popc(bal[j]);
         sm.warp_tmp[lane * NW + warp] = mine;
     }
     __syncthreads();
-    if (warp == 0) {  // scan the K*NW counts, CPL per lane
-        constexpr int CPL = (K * NW + 31) / 32;
+    if (warp == 0) {  // scan the NPT*NW counts, CPL per lane
+        constexpr int CPL = (NPT * NW + 31) / 32;
         unsigned a[CPL], sum = 0;
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
             const unsigned i = CPL * lane + q;
-            a[q] = i < K * NW ? sm.warp_tmp[i] : 0u;
+            a[q] = i < NPT * NW ? sm.warp_tmp[i] : 0u;
             sum += a[q];
         }
         const unsigned incl = warp_incl_scan(sum);
@@ -605,153 +582,22 @@ __device__ __forceinline__ unsigned compact_tile(const int *u, const bool *lost,
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
             const unsigned i = CPL * lane + q;
-            if (i < K * NW) sm.warp_tmp[i] = run;
+            if (i < NPT * NW) sm.warp_tmp[i] = run;
             run += a[q];
         }
         if (lane == 31) sm.out_cnt = incl;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < K; ++j)
+    for (int j = 0; j < NPT; ++j)
         if (lost[j]) out[written + sm.warp_tmp[j * NW + warp] + __popc(bal[j] & lanemask_lt())] = u[j];
     const unsigned tot = sm.out_cnt;
     __syncthreads();
     return tot;
 }
 
-// ------------------------------------------------------------------ staged bin-0 sweep
-// producer side (one thread): stage the X words + row offsets of tile
-// [a, a+cnt), then (once they landed) its column span
-__device__ __forceinline__ void stage_issue_a(const Params &P, const int *ro, Stage &st, StageCtl &c, int s,
-                                              long long a, unsigned cnt) {
-    const unsigned bx = (cnt * 4u + 15u) & ~15u;
-    const unsigned br = ((cnt + 1u) * 4u + 15u) & ~15u;
-    mbar_expect_tx(&c.bar_a[s], bx + br);
-    bulk_g2s(st.X, P.X + a, bx, &c.bar_a[s]);
-    bulk_g2s(st.ro, ro + a, br, &c.bar_a[s]);
-}
-
-__device__ __forceinline__ void stage_issue_b(const Params &P, Stage &st, StageCtl &c, int s, unsigned cnt,
-                                              unsigned parity, long long m) {
-    mbar_wait(&c.bar_a[s], parity);
-    const int lo = st.ro[0], hi = st.ro[cnt];
-    const int lo16 = lo & ~3;
-    const long long hi16 = ((long long)hi + 3) & ~3LL;
-    c.lo16[s] = lo16;
-    if (hi16 - lo16 <= ST_CI && hi16 <= m && hi > lo) {
-        c.ci_ok[s] = 1;
-        const unsigned bytes = (unsigned)(hi16 - lo16) * 4u;
-        mbar_expect_tx(&c.bar_b[s], bytes);
-        bulk_g2s(st.ci, P.ci + lo16, bytes, &c.bar_b[s]);
-    } else {
-        c.ci_ok[s] = 0;  // span too large (or at the array end): direct loads
-        mbar_arrive(&c.bar_b[s]);
-    }
-}
-
-template <bool STATS, int PHASE>
-__device__ __forceinline__ void staged_tile(const Params &P, const Stage &st, const StageCtl &c, int s,
-                                            long long a, unsigned cnt, int u[ST_NPT], bool lost[ST_NPT],
-                                            unsigned long long &my_conf, unsigned long long *my_edges) {
-    const bool ci_ok = c.ci_ok[s];
-    const int lo16 = c.lo16[s];
-#pragma unroll
-    for (int j = 0; j < ST_NPT; ++j) {
-        const unsigned idx = j * BLOCK + threadIdx.x;
-        lost[j] = false;
-        u[j] = -1;
-        if (idx >= cnt) continue;
-        const unsigned xu = st.X[idx];
-        if (xu & FBIT) continue;  // topology sweep: inactive (_kernels.pyx:76-77, 135-136)
-        u[j] = (int)(a + idx);
-        const int rb = st.ro[idx], re = st.ro[idx + 1];
-        if (PHASE == 0) {
-            unsigned long long mask = 0;
-            for (int k0 = rb; k0 < re; k0 += 4) {
-                int nb[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    nb[q] = k0 + q < re ? (ci_ok ? st.ci[k0 + q - lo16] : ld_col(P.ci + k0 + q)) : -1;
-                unsigned x[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const long long r = (long long)nb[q] - a;
-                    x[q] = nb[q] < 0 ? 0u : ((unsigned long long)r < cnt ? st.X[r] : P.X[nb[q]]);
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) mask_add(mask, x[q]);
-            }
-            P.X[u[j]] = (unsigned)__ffsll((long long)~mask);  // deg <= 16: a zero bit exists
-            if (STATS) my_edges[0] += re - rb;
-        } else {
-            unsigned cnt_k = 0, low = 0;
-            bool stop = false;
-            for (int k0 = rb; !stop && k0 < re; k0 += 4) {
-                int nb[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    nb[q] = k0 + q < re ? (ci_ok ? st.ci[k0 + q - lo16] : ld_col(P.ci + k0 + q)) : 0x7fffffff;
-                unsigned x[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const long long r = (long long)nb[q] - a;
-                    x[q] = nb[q] >= u[j] ? 0u : ((unsigned long long)r < cnt ? st.X[r] : P.X[nb[q]]);
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (nb[q] < u[j]) { cnt_k += (x[q] & CMASK) == xu; ++low; }
-                    else stop = true;  // adjacency sorted ascending (graph.py:193-197)
-                }
-            }
-            my_conf += cnt_k;
-            if (STATS) my_edges[1] += low;
-            lost[j] = cnt_k != 0;
-            if (!lost[j]) P.X[u[j]] = xu | FBIT;
-        }
-    }
-}
-
-// a topology-ident bin-0 chunk [lo, hi) through the staged pipeline
-template <bool STATS, int PHASE>
-__device__ void staged_chunk(const Params &P, const int *ro, Smem &sm, Stage *stages, unsigned long long lo,
-                             unsigned long long hi, int *out, unsigned &written,
-                             unsigned long long &my_conf, unsigned long long *my_edges) {
-    StageCtl &c = sm.stc;
-    const unsigned ntiles = (unsigned)((hi - lo + ST_NODES - 1) / ST_NODES);
-    const unsigned g0 = c.count;  // CTA-uniform (read after the unit barrier)
-    auto tile_cnt = [&](unsigned i) { return (unsigned)min((unsigned long long)ST_NODES, hi - (lo + (unsigned long long)i * ST_NODES)); };
-    if (threadIdx.x == 0) {
-        for (unsigned i = 0; i < ntiles && i < ST_STAGES; ++i) {
-            const unsigned g = g0 + i;
-            stage_issue_a(P, ro, stages[g % ST_STAGES], c, g % ST_STAGES, (long long)(lo + (unsigned long long)i * ST_NODES), tile_cnt(i));
-        }
-        stage_issue_b(P, stages[g0 % ST_STAGES], c, g0 % ST_STAGES, tile_cnt(0), (g0 / ST_STAGES) & 1u, P.m);
-    }
-    for (unsigned i = 0; i < ntiles; ++i) {
-        const unsigned g = g0 + i, sidx = g % ST_STAGES, parity = (g / ST_STAGES) & 1u;
-        if (threadIdx.x == 0 && i + 1 < ntiles) {
-            const unsigned g1 = g + 1;
-            stage_issue_b(P, stages[g1 % ST_STAGES], c, g1 % ST_STAGES, tile_cnt(i + 1), (g1 / ST_STAGES) & 1u, P.m);
-        }
-        mbar_wait(&c.bar_a[sidx], parity);
-        mbar_wait(&c.bar_b[sidx], parity);
-        const long long a = (long long)(lo + (unsigned long long)i * ST_NODES);
-        const unsigned cnt = tile_cnt(i);
-        int u[ST_NPT];
-        bool lost[ST_NPT];
-        staged_tile<STATS, PHASE>(P, stages[sidx], c, sidx, a, cnt, u, lost, my_conf, my_edges);
-        if (PHASE == 1) written += compact_tile<ST_NPT>(u, lost, out, written, sm);
-        else __syncthreads();  // stage sidx fully consumed
-        if (threadIdx.x == 0 && i + ST_STAGES < ntiles) {
-            fence_proxy_async();  // generic reads of the stage before the async overwrite
-            stage_issue_a(P, ro, stages[sidx], c, sidx, a + (long long)ST_STAGES * ST_NODES, tile_cnt(i + ST_STAGES));
-        }
-    }
-    if (threadIdx.x == 0) c.count = g0 + ntiles;
-}
-
 // a chunk of a group bin: warps take warp tiles of 32/G nodes round-robin
-template <int G, typename OffT, bool STATS, int PHASE>
+template <int G, typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Smem &sm, int bin,
                                             unsigned c, int np, unsigned long long &my_conf,
                                             unsigned long long *my_edges) {
@@ -765,7 +611,7 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
     __syncthreads();
     constexpr unsigned NG = 32 / G;
     for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG)
-        group_tile<G, OffT, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out,
+        group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out,
                                           &sm.out_cnt, sm.win_bm[warp], my_conf, my_edges);
     __syncthreads();
     if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][bin][c] = sm.out_cnt;
@@ -773,7 +619,7 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
 
 // One unit of one phase.  All CTA-uniform inputs come from shared memory.
 // Unit ranges: [ubase0, ubase1) hubs, then bins 3, 2, 1, 0.
-template <typename OffT, bool STATS, int PHASE>
+template <typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &sm, unsigned unit,
                                          int p, unsigned long long &my_conf,
                                          unsigned long long *my_edges) {
@@ -785,18 +631,18 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         // ---- hub (or bin-3 node in the latency regime): one CTA per node
         const unsigned c = is_hub ? unit : unit - ub[1];
         const int u = is_hub ? rc.L[BIN_HUB].base[c] : rc.L[3].base[list_index(rc.L[3], sm.prefix[3], c)];
-        const unsigned xu = P.X[u];
+        const unsigned xu = xget<F>(P, u);
         unsigned pushed = 0;
         if (!(rc.topo && (xu & FBIT))) {  // topology sweep: inactive (_kernels.pyx:76)
             if (PHASE == 0) {
-                const unsigned T = assign_cta(P, ro, u, sm);
+                const unsigned T = assign_cta<OffT, F>(P, ro, u, sm);
                 if (threadIdx.x == 0) {
-                    P.X[u] = T;
+                    xput<F>(P, u, T);
                     if (STATS) my_edges[0] += ro[u + 1] - ro[u];
                 }
             } else {
                 unsigned low;
-                const unsigned k = resolve_cta(P, ro, u, xu, sm, low);
+                const unsigned k = resolve_cta<OffT, F>(P, ro, u, xu, sm, low);
                 if (threadIdx.x == 0) {
                     my_conf += k;
                     if (STATS) my_edges[1] += low;
@@ -805,18 +651,18 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
                         else P.dyn[np][3][c] = u;  // segment c, capacity 1
                         pushed = 1;
                     } else {
-                        P.X[u] = xu | FBIT;
+                        xput<F>(P, u, xu | FBIT);
                     }
                 }
             }
         }
         if (!is_hub && PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][3][c] = pushed;
     } else if (unit < ub[2]) {
-        group_chunk<32, OffT, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
+        group_chunk<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
     } else if (unit < ub[3]) {
-        group_chunk<16, OffT, STATS, PHASE>(P, ro, sm, 2, unit - ub[2], np, my_conf, my_edges);
+        group_chunk<16, OffT, F, STATS, PHASE>(P, ro, sm, 2, unit - ub[2], np, my_conf, my_edges);
     } else if (unit < ub[4]) {
-        group_chunk<8, OffT, STATS, PHASE>(P, ro, sm, 1, unit - ub[3], np, my_conf, my_edges);
+        group_chunk<8, OffT, F, STATS, PHASE>(P, ro, sm, 1, unit - ub[3], np, my_conf, my_edges);
     } else {
         // ---- bin 0 chunk
         const unsigned c = unit - ub[4];
@@ -825,26 +671,17 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         const unsigned long long hi = min(lo + csz0, rc.L[0].total);
         int *out = P.dyn[np][0] + (long long)c * csz0;
         unsigned written = 0;
-        if constexpr (std::is_same<OffT, int>::value) {
-            if (rc.ident && P.staged) {  // contiguous tiles: bulk-async staged pipeline
-                extern __shared__ __align__(128) unsigned char dyn_smem[];
-                staged_chunk<STATS, PHASE>(P, ro, sm, reinterpret_cast<Stage *>(dyn_smem), lo, hi, out, written,
-                                           my_conf, my_edges);
-                if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
-                return;
-            }
-        }
         for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
             int u[NPT];
             bool lost[NPT];
-            small_tile<OffT, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
-            if (PHASE == 1) written += compact_tile<NPT>(u, lost, out, written, sm);
+            small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
+            if (PHASE == 1) written += compact_tile(u, lost, out, written, sm);
         }
         if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
     }
 }
 
-template <typename OffT, bool STATS, int PHASE>
+template <typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem &sm, int p,
                                           unsigned long long &my_conf, unsigned long long *my_edges) {
     unsigned *ctr = &P.ctrl->unit_ctr[PHASE][p];
@@ -854,7 +691,7 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem 
     __syncthreads();
     while (unit < sm.rc.ubase[NBIN]) {
         if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);  // prefetch the next unit
-        run_unit<OffT, STATS, PHASE>(P, ro, sm, unit, p, my_conf, my_edges);
+        run_unit<OffT, F, STATS, PHASE>(P, ro, sm, unit, p, my_conf, my_edges);
         __syncthreads();
         unit = sm.unit;
         __syncthreads();
@@ -862,7 +699,7 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem 
 }
 
 // ------------------------------------------------------------------ kernel
-template <typename OffT, bool STATS>
+template <typename OffT, class F, bool STATS>
 __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
     __shared__ Smem sm;
     Ctrl *C = P.ctrl;
@@ -873,7 +710,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
     const long long gthreads = (long long)P.nblocks * BLOCK;
     RoundCfg &rc = sm.rc;
 
-    for (long long u = gtid; u < P.n; u += gthreads) P.X[u] = 0u;
+    for (long long u = gtid; u < P.n; u += gthreads) xput<F>(P, u, 0u);
     if (threadIdx.x == 0) {
         unsigned long long off = 0;
         for (int b = 0; b < NBIN; ++b) {
@@ -883,12 +720,6 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         }
         rc.ident_small = rc.nst[0] == (unsigned long long)P.n;  // all nodes in bin 0: sweep ids
         for (int b = 0; b < NSEG_BINS; ++b) rc.prev_nseg[b] = rc.prev_cap[b] = 0;
-        for (int st = 0; st < ST_STAGES; ++st) {
-            mbar_init(&sm.stc.bar_a[st], 1);
-            mbar_init(&sm.stc.bar_b[st], 1);
-        }
-        sm.stc.count = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     grid_sync(&C->bar, P.nblocks);
 
@@ -1001,9 +832,9 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         __syncthreads();
         if (s == 0) break;  // worklist drained (driver.py:145)
 
-        run_phase<OffT, STATS, 0>(P, ro, sm, p, my_conf, my_edges);
+        run_phase<OffT, F, STATS, 0>(P, ro, sm, p, my_conf, my_edges);
         grid_sync(&C->bar, P.nblocks);
-        run_phase<OffT, STATS, 1>(P, ro, sm, p, my_conf, my_edges);
+        run_phase<OffT, F, STATS, 1>(P, ro, sm, p, my_conf, my_edges);
 
         // conflicts of this round: block reduce then one atomic per CTA
         {
@@ -1034,7 +865,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         C->rounds = t - 1;
         if (t - 1 > P.max_rec) C->rec_overflow = 1;
     }
-    for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(P.X[u] & CMASK);
+    for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(xget<F>(P, u) & CMASK);
 }
 
 // Static lists: nodes bucket-sorted by a degree key.  Keys 0-2 are bins 0-2;
@@ -1073,61 +904,82 @@ __global__ void narrow_offsets_kernel(const long long *ro, int *ro32, long long 
         ro32[i] = (int)ro[i];
 }
 
+// int16 delta columns ci16[k] = ci[k] - u; sets *bad when some |v-u| >= 2^15
+// (then the absolute int32 columns are used).  Warp per row, early exit.
+__global__ void delta_columns_kernel(const long long *ro, const int *ci, long long n, short *ci16,
+                                     unsigned *bad) {
+    const unsigned lane = lane_id();
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
+        if (*(volatile unsigned *)bad) return;
+        bool over = false;
+        for (long long k = ro[u] + lane; k < ro[u + 1]; k += 32) {
+            const long long d = (long long)ci[k] - u;
+            over |= d < -32768 || d > 32767;
+            ci16[k] = (short)d;
+        }
+        if (__any_sync(FULL, over)) {
+            if (lane == 0) atomicOr(bad, 1u);
+            return;
+        }
+    }
+}
+
 // worst-case segmented capacity of a bin with `cnt` static nodes
 inline size_t seg_capacity(long long cnt) {
     return (size_t)cnt + (size_t)cnt / MAXSEG + 2 * BLOCK * NPT;
 }
 
 struct Layout {
-    size_t x, stat, dyn[2][NBIN], ro32, ctrl, part, total;
+    size_t x, stat, dyn[2][NBIN], ro32, ci16, ctrl, part, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
 // the device; size each for the whole node count (upper bound of every bin).
-static Layout layout(long long n) {
+static Layout layout(long long n, long long m) {
     Layout L;
     size_t o = 0;
-    L.x = o; o = align_up(o + 4 * (size_t)n + 64, 256);  // +pad: 16-byte bulk copies of the tail tile
+    L.x = o; o = align_up(o + 4 * (size_t)n, 256);
     L.stat = o; o = align_up(o + 4 * (size_t)n, 256);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) {
             L.dyn[p][b] = o;
             o = align_up(o + 4 * (b == BIN_HUB ? (size_t)n : seg_capacity(n)), 256);
         }
-    L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1) + 64, 256);
+    L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
+    L.ci16 = o; o = align_up(o + (m < 0x7fffffffLL ? 2 * (size_t)m : 0) + 256, 256);
     L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
     L.part = o; o = align_up(o + part_scratch_bytes(NKEY, n), 256);
     L.total = o;
     return L;
 }
 
-template <typename OffT, bool STATS>
+template <typename OffT, class F, bool STATS>
 static const void *kernel_ptr() {
-    return (const void *)solve_kernel<OffT, STATS>;
+    return (const void *)solve_kernel<OffT, F, STATS>;
 }
 
-static bool configure_smem() {
-    static bool done = false;
-    if (!done) {
-        for (const void *fn : {kernel_ptr<int, false>(), kernel_ptr<int, true>()})
-            if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)STAGE_SMEM) !=
-                cudaSuccess)
-                return false;
-        done = true;
-    }
-    return true;
+// the instantiation for (offset width, state width, column format, stats)
+static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats) {
+    if (!narrow) return stats ? kernel_ptr<long long, F32, true>() : kernel_ptr<long long, F32, false>();
+    if (x16 && c16) return stats ? kernel_ptr<int, F16D, true>() : kernel_ptr<int, F16D, false>();
+    if (x16) return stats ? kernel_ptr<int, F16, true>() : kernel_ptr<int, F16, false>();
+    if (c16) return stats ? kernel_ptr<int, F32D, true>() : kernel_ptr<int, F32D, false>();
+    return stats ? kernel_ptr<int, F32, true>() : kernel_ptr<int, F32, false>();
 }
 
-static int occupancy(bool staged = false) {
-    int per_sm = 0, per_sm64 = 0;
-    if (!configure_smem()) return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, solve_kernel<int, false>, BLOCK,
-                                                      staged ? STAGE_SMEM : 0) != cudaSuccess)
-        return 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm64, solve_kernel<long long, false>, BLOCK, 0) !=
-        cudaSuccess)
-        return 0;
-    return std::min(per_sm, per_sm64);
+static int occupancy_of(const void *fn) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, 0) != cudaSuccess) return 0;
+    return per_sm;
+}
+
+static int occupancy() {
+    int lo = 1 << 30;
+    for (bool n : {false, true})
+        for (bool x : {false, true})
+            for (bool c : {false, true}) lo = std::min(lo, occupancy_of(select_kernel(n, x, c, false)));
+    return lo;
 }
 
 }  // namespace solve
@@ -1146,7 +998,7 @@ int hc_device_info(int *h_num_sms, int *h_ctas_per_sm) {
 
 size_t hc_solve_workspace_bytes(int64_t num_nodes, int64_t num_edges) {
     (void)num_edges;
-    return layout(num_nodes < 0 ? 0 : num_nodes).total;
+    return layout(num_nodes < 0 ? 0 : num_nodes, num_edges < 0 ? 0 : num_edges).total;
 }
 
 int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
@@ -1171,7 +1023,7 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     if (num_nodes == 0) return HC_OK;  // empty graph: 0 rounds (test_driver.py:88-93)
     HC_REQUIRE(d_row_offsets && d_colors && (num_edges == 0 || d_col_indices), HC_ERR_INVALID,
                "hc_solve: null pointer");
-    const Layout L = layout(num_nodes);
+    const Layout L = layout(num_nodes, num_edges);
     HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
                "hc_solve: workspace %zu bytes < required %zu", ws_bytes, L.total);
     char *ws = reinterpret_cast<char *>(d_ws);
@@ -1191,7 +1043,6 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     P.mode = mode;
     P.thr = thr_count;
     P.stats = reinterpret_cast<long long *>(d_stats);
-    P.m = num_edges;
     if (d_stats && P.max_rec)
         HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
 
@@ -1210,23 +1061,30 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
         HC_CHECK_LAUNCH();
     }
 
-    // Staged sweeps need shared memory that would otherwise be L1: reserve it
-    // only when every node is in bin 0 (the sweeps can then stage tiles).
-    bool staged = false;
-    if (narrow && HC_STAGE) {
-        unsigned long long nst0 = 0;
-        HC_CUDA_TRY(cudaMemcpyAsync(&nst0, &P.ctrl->nstat[0], sizeof nst0, cudaMemcpyDeviceToHost, st));
-        HC_CUDA_TRY(cudaStreamSynchronize(st));
-        staged = nst0 == (unsigned long long)num_nodes;
+    // storage formats (see Fmt): 16-bit state words when max degree <= 16384
+    // (no node in the hub buckets >= 16385), 16-bit delta columns when every
+    // |v - u| < 2^15
+    unsigned long long h_tot[NKEY];
+    unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? 2 * (size_t)num_edges : 0));
+    HC_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
+    P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
+    if (narrow && num_edges > 0) {
+        delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro64, d_col_indices, num_nodes,
+                                                      reinterpret_cast<short *>(ws + L.ci16), bad);
+        HC_CHECK_LAUNCH();
     }
-    P.staged = staged ? 1 : 0;
-    const int per_sm = occupancy(staged);
+    unsigned h_bad = 1;
+    HC_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    const bool x16 = (HC_FMT16 != 0) && h_tot[9] + h_tot[10] + h_tot[11] + h_tot[12] == 0;
+    const bool c16 = (HC_FMT16 != 0) && narrow && num_edges > 0 && h_bad == 0;
+    const int per_sm = occupancy();
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * sms);
     void *args[] = {&P};
-    const void *fn = narrow ? (d_stats ? kernel_ptr<int, true>() : kernel_ptr<int, false>())
-                            : (d_stats ? kernel_ptr<long long, true>() : kernel_ptr<long long, false>());
-    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, staged ? STAGE_SMEM : 0, st));
+    const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr);
+    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
     long long info[2];
     HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));

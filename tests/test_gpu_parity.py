@@ -236,3 +236,19 @@ def test_worklist_semantics():
         wl2.push(1)
     with pytest.raises(RuntimeError):
         wl2.push(7)
+
+
+@pytest.mark.parametrize("leaves,extra", [(20000, 3000), (40000, 5000), (3000, 200000)])
+def test_storage_formats_vs_oracle(leaves, extra):
+    """Star hubs push the solve onto each storage format: 32-bit state words
+    (a degree > 16384), int32 vs int16-delta columns (|v-u| >= 2^15 or not)."""
+    rng = np.random.default_rng(leaves)
+    n = leaves + 1
+    e = np.concatenate([np.column_stack([np.zeros(leaves, np.int64), np.arange(1, n)]),
+                        rng.integers(0, n, (extra, 2))])
+    ro, ci = O.build_csr(n, e)
+    g = hc.CsrGraph(n, len(ci), ro, ci)
+    for mode in MODES:
+        want, rec = O.color(ro, ci, mode)
+        colors, rep = hc.color_graph(g, hc.HybridConfig(mode=mode))
+        assert np.array_equal(colors, want) and np.array_equal(_recs(rep), rec), mode
