@@ -217,21 +217,20 @@ using F16 = Fmt<unsigned short, int>;
 using F16D = Fmt<unsigned short, short>;
 using F32D = Fmt<unsigned, short>;
 
+// committed flag / color mask of the format's state word; words are kept
+// zero-extended in registers, so no conversion on load or store
+template <class F>
+constexpr unsigned FB = sizeof(typename F::xt) == 4 ? 0x80000000u : 0x8000u;
+template <class F>
+constexpr unsigned CM = FB<F> - 1u;
+
 template <class F>
 __device__ __forceinline__ unsigned xget(const Params &P, long long v) {
-    if constexpr (sizeof(typename F::xt) == 4) {
-        return reinterpret_cast<const unsigned *>(P.X)[v];
-    } else {
-        const unsigned s = reinterpret_cast<const unsigned short *>(P.X)[v];
-        return ((s & 0x8000u) << 16) | (s & 0x7fffu);
-    }
+    return reinterpret_cast<const typename F::xt *>(P.X)[v];
 }
 template <class F>
 __device__ __forceinline__ void xput(const Params &P, long long v, unsigned w) {
-    if constexpr (sizeof(typename F::xt) == 4)
-        reinterpret_cast<unsigned *>(P.X)[v] = w;
-    else
-        reinterpret_cast<unsigned short *>(P.X)[v] = (unsigned short)(((w >> 16) & 0x8000u) | (w & 0x7fffu));
+    reinterpret_cast<typename F::xt *>(P.X)[v] = (typename F::xt)w;
 }
 // streaming load of a column id (evict-first so the X gathers keep L2)
 template <class F>
@@ -242,9 +241,10 @@ __device__ __forceinline__ int colget(const Params &P, long long k, int u) {
         return u + (int)__ldcs(P.ci16 + k);
 }
 
+template <class F>
 __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
-    const unsigned c = x & CMASK;
-    if ((x & FBIT) && c <= 64u) mask |= 1ull << (c - 1u);
+    const unsigned c = x & CM<F>;
+    if ((x & FB<F>) && c <= 64u) mask |= 1ull << (c - 1u);
 }
 
 // ------------------------------------------------------------------ groups
@@ -260,8 +260,8 @@ __device__ unsigned warp_mex_above64(const Params &P, int u, long long b, long l
         const unsigned hi = min(lim, w0 + WIN_WORDS * 32);
         for (long long k = b + lane; k < e; k += 32) {
             const unsigned x = xget<F>(P, colget<F>(P, k, u));
-            const unsigned c = x & CMASK;
-            if ((x & FBIT) && c > w0 && c <= hi) mark(bm, c - w0);
+            const unsigned c = x & CM<F>;
+            if ((x & FB<F>) && c > w0 && c <= hi) mark(bm, c - w0);
         }
         __syncwarp();
         const unsigned word = bm[lane];
@@ -288,7 +288,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     unsigned xu = 0;
     if (topo || PHASE == 1) {
         xu = u >= 0 ? xget<F>(P, u) : 0u;
-        if (topo && (xu & FBIT)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
+        if (topo && (xu & FB<F>)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
     }
     const long long b = u >= 0 ? (long long)ro[u] : 0, e = u >= 0 ? (long long)ro[u + 1] : 0;
     unsigned iters = (unsigned)((e - b + 4 * G - 1) / (4 * G));
@@ -318,7 +318,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
             for (int q = 0; q < 4; ++q) x[q] = nb[q] >= 0 ? xget<F>(P, nb[q]) : 0u;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) mask_add(mask, x[q]);
+            for (int q = 0; q < 4; ++q) mask_add<F>(mask, x[q]);
         } else {
             unsigned x[4];
 #pragma unroll
@@ -326,7 +326,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             bool ge = false;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (nb[q] < u) { cnt += (x[q] & CMASK) == xu; ++low; }
+                if (nb[q] < u) { cnt += (x[q] & CM<F>) == xu; ++low; }
                 else if (nb[q] != 0x7fffffff) ge = true;
             }
             // adjacency sorted ascending (graph.py:193-197): once any lane of the
@@ -369,7 +369,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             my_conf += cnt;
             if (STATS) my_edges[1] += low;
             if (cnt) out[atomicAdd(out_cnt, 1u)] = u;
-            else xput<F>(P, u, xu | FBIT);
+            else xput<F>(P, u, xu | FB<F>);
         }
     }
 }
@@ -393,8 +393,8 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
             for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                const unsigned c = x[q] & CMASK;
-                if ((x[q] & FBIT) && c > w0 && c <= hi) mark(sm.hub_bm, c - w0);
+                const unsigned c = x[q] & CM<F>;
+                if ((x[q] & FB<F>) && c > w0 && c <= hi) mark(sm.hub_bm, c - w0);
             }
         }
         __syncthreads();
@@ -432,7 +432,7 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
         bool stop = false;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            if (v[q] < u) { cnt += (x[q] & CMASK) == T; ++low; }
+            if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
             else stop = true;
         }
         if (__any_sync(FULL, stop)) break;  // later chunks are all >= u
@@ -481,7 +481,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
         if (topo) {
 #pragma unroll
             for (int j = 0; j < NPT; ++j)
-                if (xu[j] & FBIT) { u[j] = -1; re[j] = rb[j]; }  // inactive (_kernels.pyx:76-77, 135-136)
+                if (xu[j] & FB<F>) { u[j] = -1; re[j] = rb[j]; }  // inactive (_kernels.pyx:76-77, 135-136)
         }
     }
     int nb[NPT][4];
@@ -500,7 +500,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
             if (u[j] < 0) continue;
             unsigned long long mask = 0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) mask_add(mask, x[j][q]);
+            for (int q = 0; q < 4; ++q) mask_add<F>(mask, x[j][q]);
             for (OffT k = rb[j] + 4; k < re[j]; k += 4) {  // deg 5..16
                 int v2[4];
                 unsigned x2[4];
@@ -509,7 +509,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
                 for (int q = 0; q < 4; ++q) x2[q] = v2[q] >= 0 ? xget<F>(P, v2[q]) : 0u;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) mask_add(mask, x2[q]);
+                for (int q = 0; q < 4; ++q) mask_add<F>(mask, x2[q]);
             }
             xput<F>(P, u[j], (unsigned)__ffsll((long long)~mask));  // deg <= 16: a zero bit exists
             if (STATS) my_edges[0] += re[j] - rb[j];
@@ -528,7 +528,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
             bool stop = false;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (nb[j][q] >= 0 && nb[j][q] < u[j]) { cnt += (x[j][q] & CMASK) == T; ++low; }
+                if (nb[j][q] >= 0 && nb[j][q] < u[j]) { cnt += (x[j][q] & CM<F>) == T; ++low; }
                 else stop = true;
             }
             for (OffT k = rb[j] + 4; !stop && k < re[j]; k += 4) {
@@ -540,14 +540,14 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
                 for (int q = 0; q < 4; ++q) x2[q] = v2[q] < u[j] ? xget<F>(P, v2[q]) : 0u;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    if (v2[q] < u[j]) { cnt += (x2[q] & CMASK) == T; ++low; }
+                    if (v2[q] < u[j]) { cnt += (x2[q] & CM<F>) == T; ++low; }
                     else stop = true;  // adjacency sorted ascending (graph.py:193-197)
                 }
             }
             my_conf += cnt;
             if (STATS) my_edges[1] += low;
             lost[j] = cnt != 0;
-            if (!lost[j]) xput<F>(P, u[j], T | FBIT);
+            if (!lost[j]) xput<F>(P, u[j], T | FB<F>);
         }
     }
 }
@@ -633,7 +633,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         const int u = is_hub ? rc.L[BIN_HUB].base[c] : rc.L[3].base[list_index(rc.L[3], sm.prefix[3], c)];
         const unsigned xu = xget<F>(P, u);
         unsigned pushed = 0;
-        if (!(rc.topo && (xu & FBIT))) {  // topology sweep: inactive (_kernels.pyx:76)
+        if (!(rc.topo && (xu & FB<F>))) {  // topology sweep: inactive (_kernels.pyx:76)
             if (PHASE == 0) {
                 const unsigned T = assign_cta<OffT, F>(P, ro, u, sm);
                 if (threadIdx.x == 0) {
@@ -651,7 +651,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
                         else P.dyn[np][3][c] = u;  // segment c, capacity 1
                         pushed = 1;
                     } else {
-                        xput<F>(P, u, xu | FBIT);
+                        xput<F>(P, u, xu | FB<F>);
                     }
                 }
             }
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         C->rounds = t - 1;
         if (t - 1 > P.max_rec) C->rec_overflow = 1;
     }
-    for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(xget<F>(P, u) & CMASK);
+    for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(xget<F>(P, u) & CM<F>);
 }
 
 // Static lists: nodes bucket-sorted by a degree key.  Keys 0-2 are bins 0-2;
