@@ -125,6 +125,10 @@ int hc_wl_swap_and_sort(const int64_t *d_next, const int64_t *d_cursor, int64_t 
  * *h_rounds = total rounds.  If rounds > max_rec the solve still completes,
  * the first max_rec records are kept and HC_ERR_RECORDS is returned. */
 size_t hc_solve_workspace_bytes(int64_t num_nodes, int64_t num_edges);
+/* Storage-format overrides for tests and experiments (process-wide):
+ * force int64 row offsets, forbid 16-bit state words, forbid 16-bit delta
+ * columns.  Defaults (0, 0, 0) let hc_solve pick per graph. */
+int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16);
 int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
              int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
              hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, void *d_ws,

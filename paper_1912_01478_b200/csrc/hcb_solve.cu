@@ -982,6 +982,10 @@ static int occupancy() {
     return lo;
 }
 
+// format overrides (tests / experiments): force int64 offsets, forbid the
+// 16-bit state word, forbid 16-bit delta columns
+static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0;
+
 }  // namespace solve
 }  // namespace hcb
 
@@ -989,6 +993,13 @@ using namespace hcb;
 using namespace hcb::solve;
 
 extern "C" {
+
+int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16) {
+    g_force_wide = force_wide_offsets;
+    g_no_x16 = no_x16;
+    g_no_c16 = no_c16;
+    return HC_OK;
+}
 
 int hc_device_info(int *h_num_sms, int *h_ctas_per_sm) {
     if (h_num_sms) *h_num_sms = num_sms();
@@ -1027,7 +1038,7 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
                "hc_solve: workspace %zu bytes < required %zu", ws_bytes, L.total);
     char *ws = reinterpret_cast<char *>(d_ws);
-    const bool narrow = num_edges < 0x7fffffffLL;
+    const bool narrow = num_edges < 0x7fffffffLL && !g_force_wide;
     Params P;
     P.ro = narrow ? (const void *)(ws + L.ro32) : (const void *)d_row_offsets;
     P.ci = d_col_indices;
@@ -1077,8 +1088,8 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     HC_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
-    const bool x16 = (HC_FMT16 != 0) && h_tot[9] + h_tot[10] + h_tot[11] + h_tot[12] == 0;
-    const bool c16 = (HC_FMT16 != 0) && narrow && num_edges > 0 && h_bad == 0;
+    const bool x16 = (HC_FMT16 != 0) && !g_no_x16 && h_tot[9] + h_tot[10] + h_tot[11] + h_tot[12] == 0;
+    const bool c16 = (HC_FMT16 != 0) && !g_no_c16 && narrow && num_edges > 0 && h_bad == 0;
     const int per_sm = occupancy();
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * sms);
