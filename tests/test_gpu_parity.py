@@ -252,3 +252,22 @@ def test_storage_formats_vs_oracle(leaves, extra):
         want, rec = O.color(ro, ci, mode)
         colors, rep = hc.color_graph(g, hc.HybridConfig(mode=mode))
         assert np.array_equal(colors, want) and np.array_equal(_recs(rep), rec), mode
+
+
+@pytest.mark.parametrize("fmt", [(1, 1, 1), (0, 1, 1), (0, 0, 1), (0, 1, 0)])
+def test_forced_storage_formats_vs_golden(configs, fmt):
+    """Every (offset width, state width, column format) instantiation on the
+    reference-recorded C1 graph (RMAT-16) and a grid."""
+    L = hc._lib.load()
+    L.hc_solve_set_formats(*fmt)
+    try:
+        for key in ("rmat16", "grid64x96"):
+            kind, kw = CONFIG_SPECS[key]
+            want = configs[key]
+            dg = _device_graph(kind, kw)
+            for mode in MODES:
+                colors, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+                assert np.array_equal(colors, want["colors"]), (key, mode, fmt)
+                assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt)
+    finally:
+        L.hc_solve_set_formats(0, 0, 0)
