@@ -165,6 +165,18 @@ int hc_dist_apply(uint32_t *d_X, const int32_t *d_ids, const uint32_t *d_vals, i
 int hc_dist_colors(const uint32_t *d_X, int64_t lo, int64_t hi, int64_t *d_colors, void *stream);
 
 /* ------------------------------------------------------------------ */
+/* §3 micro-benchmark pair (bench.py:67-161, _kernels.pyx:152-187):     */
+/* one persistent kernel runs the whole pipe of `variant` (0 push_wl,   */
+/* 1 push_nowl) over n nodes deactivating `batch` lowest-id active     */
+/* nodes per iteration; per iteration it records the push phase's      */
+/* device nanoseconds, the worklist size before, and the cutoff id.    */
+/* ------------------------------------------------------------------ */
+size_t hc_push_bench_workspace_bytes(int64_t num_nodes);
+int hc_push_bench(int64_t num_nodes, int64_t batch, int variant, int64_t *d_rec_ns, int64_t *d_rec_size,
+                  int64_t *d_rec_cutoff, int64_t max_iters, int64_t *h_iters, void *d_ws, size_t ws_bytes,
+                  void *stream);
+
+/* ------------------------------------------------------------------ */
 /* Graph construction / generators / verification.                      */
 /* ------------------------------------------------------------------ */
 

@@ -80,6 +80,8 @@ _SIGS = {
     "hc_dist_resolve": (ctypes.c_int, [_p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
     "hc_dist_apply": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
     "hc_dist_colors": (ctypes.c_int, [_p, _i64, _i64, _p, _p]),
+    "hc_push_bench_workspace_bytes": (ctypes.c_size_t, [_i64]),
+    "hc_push_bench": (ctypes.c_int, [_i64, _i64, ctypes.c_int, _p, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_build_csr_workspace_bytes": (ctypes.c_size_t, [_i64, _i64]),
     "hc_build_csr": (ctypes.c_int, [_p, _i64, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),
     "hc_gen_grid": (ctypes.c_int, [_i64, _i64, _p, _p]),
