@@ -24,6 +24,8 @@ namespace pushbench {
 constexpr int BLOCK = 512;
 constexpr int NW = BLOCK / 32;
 constexpr int MAXG = 512;  // max CTAs (segments)
+constexpr int EPT = 16;    // elements per thread per tile
+static_assert(EPT * NW % 32 == 0, "scan layout");
 
 struct Ctrl {
     GridBarrier bar;
@@ -48,6 +50,7 @@ struct Params {
 struct Smem {
     unsigned prefix[MAXG + 1];
     unsigned warp_tmp[NW];
+    unsigned jw[EPT * NW];
     unsigned tot;
     long long cutoff;
 };
@@ -70,20 +73,20 @@ __device__ __forceinline__ unsigned seg_of(const Smem &sm, unsigned nseg, unsign
     return lo;
 }
 
-// block-ordered compaction: returns this thread's rank among set flags
-__device__ __forceinline__ unsigned block_rank(bool f, unsigned &total, Smem &sm) {
+// block exclusive sum of one value per thread; *total = sum
+__device__ __forceinline__ unsigned block_excl_sum(unsigned x, unsigned &total, Smem &sm) {
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    const unsigned bal = __ballot_sync(FULL, f);
-    if (lane == 0) sm.warp_tmp[warp] = __popc(bal);
+    const unsigned incl = warp_incl_scan(x);
+    if (lane == 31) sm.warp_tmp[warp] = incl;
     __syncthreads();
     if (warp == 0) {
         const unsigned v = lane < NW ? sm.warp_tmp[lane] : 0u;
-        const unsigned incl = warp_incl_scan(v);
-        if (lane < NW) sm.warp_tmp[lane] = incl - v;
-        if (lane == 31) sm.tot = incl;
+        const unsigned vi = warp_incl_scan(v);
+        if (lane < NW) sm.warp_tmp[lane] = vi - v;
+        if (lane == 31) sm.tot = vi;
     }
     __syncthreads();
-    const unsigned r = sm.warp_tmp[warp] + __popc(bal & lanemask_lt());
+    const unsigned r = sm.warp_tmp[warp] + incl - x;
     total = sm.tot;
     __syncthreads();
     return r;
@@ -127,29 +130,89 @@ __global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
         if (blockIdx.x == 0 && threadIdx.x == 0) t0 = globaltimer();
         // ---- timed push phase
         const unsigned long long span = P.variant == 0 ? size : (unsigned long long)P.n;
-        const unsigned long long lo = span * blockIdx.x / G, hi = span * (blockIdx.x + 1) / G;
+        // CTA shares rounded to 16 elements (aligned 16-byte flag loads)
+        const unsigned long long lo = blockIdx.x == 0 ? 0 : ((span * blockIdx.x / G) & ~15ull);
+        const unsigned long long hi = blockIdx.x + 1 == G ? span : ((span * (blockIdx.x + 1) / G) & ~15ull);
         int *out = P.seg[np] + (long long)blockIdx.x * P.segcap;
         unsigned written = 0;
-        unsigned s = (P.variant == 0 && !dense) ? seg_of(sm, G, lo < size ? lo : 0) : 0u;
-        for (unsigned long long base = lo; base < hi; base += BLOCK) {
-            const unsigned long long v = base + threadIdx.x;
-            bool keep = false;
-            int u = -1;
-            if (v < hi) {
-                if (P.variant == 0) {  // push_wl: bench_from_list (_kernels.pyx:152-168)
-                    u = list_at(P, sm, p, dense, v, s);
-                    if (u <= cutoff) P.active[u] = 0;
-                    else keep = true;
-                } else if (P.active[v]) {  // push_nowl: bench_sweep (_kernels.pyx:171-187)
-                    u = (int)v;
-                    if (u <= cutoff) P.active[u] = 0;
-                    else keep = true;
+        if (P.variant == 1) {
+            // push_nowl, bench_sweep (_kernels.pyx:171-187): EPT consecutive
+            // ids per thread, one 16-byte load of their active flags
+            for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * EPT) {
+                const unsigned long long v0 = base + (unsigned long long)threadIdx.x * EPT;
+                unsigned keepmask = 0;
+                if (v0 < hi) {
+                    const unsigned cnt = (unsigned)min((unsigned long long)EPT, hi - v0);
+                    unsigned char f[EPT];
+                    if (cnt == EPT) {
+                        const uint4 w = *reinterpret_cast<const uint4 *>(P.active + v0);
+                        memcpy(f, &w, EPT);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < EPT; ++j) f[j] = (unsigned)j < cnt ? P.active[v0 + j] : 0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < EPT; ++j) {
+                        if (f[j]) {
+                            if ((long long)(v0 + j) <= cutoff) P.active[v0 + j] = 0;
+                            else keepmask |= 1u << j;
+                        }
+                    }
                 }
+                unsigned tot;
+                unsigned r = block_excl_sum((unsigned)__popc(keepmask), tot, sm);
+#pragma unroll
+                for (int j = 0; j < EPT; ++j)
+                    if (keepmask & (1u << j)) out[written + r++] = (int)(v0 + j);
+                written += tot;
             }
-            unsigned tot;
-            const unsigned r = block_rank(keep, tot, sm);
-            if (keep) out[written + r] = u;
-            written += tot;
+        } else {
+            // push_wl, bench_from_list (_kernels.pyx:152-168): coalesced strided
+            // reads of the list (element base + j*BLOCK + tid), j-major
+            // order-preserving compaction
+            const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+            unsigned s = dense ? 0u : seg_of(sm, G, lo < size ? lo : 0);
+            for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * EPT) {
+                int ids[EPT];
+                unsigned bal[EPT];
+#pragma unroll
+                for (int j = 0; j < EPT; ++j) {
+                    const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
+                    bool keep = false;
+                    ids[j] = 0;
+                    if (v < hi) {
+                        ids[j] = list_at(P, sm, p, dense, v, s);
+                        if (ids[j] <= cutoff) P.active[ids[j]] = 0;
+                        else keep = true;
+                    }
+                    bal[j] = __ballot_sync(FULL, keep);
+                }
+                if (lane < EPT) {
+                    unsigned mine = 0;
+#pragma unroll
+                    for (int j = 0; j < EPT; ++j)
+                        if (lane == (unsigned)j) mine = __popc(bal[j]);
+                    sm.jw[lane * NW + warp] = mine;
+                }
+                __syncthreads();
+                if (warp == 0) {  // scan EPT*NW counts in (j, warp) order, CPL per lane
+                    constexpr int CPL = EPT * NW / 32;
+                    unsigned a[CPL], sum = 0;
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) { a[q] = sm.jw[CPL * lane + q]; sum += a[q]; }
+                    const unsigned incl = warp_incl_scan(sum);
+                    unsigned run = incl - sum;
+#pragma unroll
+                    for (int q = 0; q < CPL; ++q) { sm.jw[CPL * lane + q] = run; run += a[q]; }
+                    if (lane == 31) sm.tot = incl;
+                }
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < EPT; ++j)
+                    if (bal[j] & (1u << lane)) out[written + sm.jw[j * NW + warp] + __popc(bal[j] & lanemask_lt())] = ids[j];
+                written += sm.tot;
+                __syncthreads();
+            }
         }
         if (threadIdx.x == 0) C->segcnt[np][blockIdx.x] = written;
         grid_sync(&C->bar, G);
