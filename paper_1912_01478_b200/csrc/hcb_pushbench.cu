@@ -234,6 +234,9 @@ __global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
 using namespace hcb;
 using namespace hcb::pushbench;
 
+// G segments of capacity ceil(n/G) + 16 (shares are rounded to 16 elements)
+static size_t seg_region_bytes(long long n) { return 4 * ((size_t)n + (size_t)MAXG * 32); }
+
 static unsigned pb_grid() {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pushbench_kernel, BLOCK, 0);
@@ -246,9 +249,7 @@ extern "C" {
 
 size_t hc_push_bench_workspace_bytes(int64_t n) {
     if (n < 0) n = 0;
-    const unsigned G = MAXG;
-    const size_t segcap = (size_t)((n + G - 1) / G) + 1;
-    return align_up((size_t)n + 16, 256) + 2 * align_up(4 * segcap * G, 256) + align_up(sizeof(Ctrl), 256);
+    return align_up((size_t)n + 16, 256) + 2 * align_up(seg_region_bytes(n), 256) + align_up(sizeof(Ctrl), 256);
 }
 
 int hc_push_bench(int64_t n, int64_t batch, int variant, int64_t *d_rec_ns, int64_t *d_rec_size,
@@ -268,8 +269,8 @@ int hc_push_bench(int64_t n, int64_t batch, int variant, int64_t *d_rec_ns, int6
     P.batch = batch;
     P.variant = variant;
     P.active = reinterpret_cast<unsigned char *>(ws);
-    P.segcap = (n + G - 1) / G + 1;
-    const size_t seg_bytes = align_up(4 * (size_t)P.segcap * MAXG, 256);
+    P.segcap = (n + G - 1) / G + 16;
+    const size_t seg_bytes = align_up(seg_region_bytes(n), 256);
     P.seg[0] = reinterpret_cast<int *>(ws + align_up((size_t)n + 16, 256));
     P.seg[1] = reinterpret_cast<int *>(ws + align_up((size_t)n + 16, 256) + seg_bytes);
     P.ctrl = reinterpret_cast<Ctrl *>(ws + align_up((size_t)n + 16, 256) + 2 * seg_bytes);
