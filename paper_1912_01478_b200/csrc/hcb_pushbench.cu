@@ -135,43 +135,13 @@ __global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
         const unsigned long long hi = blockIdx.x + 1 == G ? span : ((span * (blockIdx.x + 1) / G) & ~15ull);
         int *out = P.seg[np] + (long long)blockIdx.x * P.segcap;
         unsigned written = 0;
-        if (P.variant == 1) {
-            // push_nowl, bench_sweep (_kernels.pyx:171-187): EPT consecutive
-            // ids per thread, one 16-byte load of their active flags
-            for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * EPT) {
-                const unsigned long long v0 = base + (unsigned long long)threadIdx.x * EPT;
-                unsigned keepmask = 0;
-                if (v0 < hi) {
-                    const unsigned cnt = (unsigned)min((unsigned long long)EPT, hi - v0);
-                    unsigned char f[EPT];
-                    if (cnt == EPT) {
-                        const uint4 w = *reinterpret_cast<const uint4 *>(P.active + v0);
-                        memcpy(f, &w, EPT);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < EPT; ++j) f[j] = (unsigned)j < cnt ? P.active[v0 + j] : 0;
-                    }
-#pragma unroll
-                    for (int j = 0; j < EPT; ++j) {
-                        if (f[j]) {
-                            if ((long long)(v0 + j) <= cutoff) P.active[v0 + j] = 0;
-                            else keepmask |= 1u << j;
-                        }
-                    }
-                }
-                unsigned tot;
-                unsigned r = block_excl_sum((unsigned)__popc(keepmask), tot, sm);
-#pragma unroll
-                for (int j = 0; j < EPT; ++j)
-                    if (keepmask & (1u << j)) out[written + r++] = (int)(v0 + j);
-                written += tot;
-            }
-        } else {
-            // push_wl, bench_from_list (_kernels.pyx:152-168): coalesced strided
-            // reads of the list (element base + j*BLOCK + tid), j-major
-            // order-preserving compaction
+        {
+            // element v = base + j*BLOCK + tid: coalesced reads of the flags
+            // (push_nowl) or the list (push_wl), coalesced j-major
+            // order-preserving compaction of the survivors
             const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-            unsigned s = dense ? 0u : seg_of(sm, G, lo < size ? lo : 0);
+            const bool wl = P.variant == 0;
+            unsigned s = (wl && !dense) ? seg_of(sm, G, lo < size ? lo : 0) : 0u;
             for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * EPT) {
                 int ids[EPT];
                 unsigned bal[EPT];
@@ -181,9 +151,15 @@ __global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
                     bool keep = false;
                     ids[j] = 0;
                     if (v < hi) {
-                        ids[j] = list_at(P, sm, p, dense, v, s);
-                        if (ids[j] <= cutoff) P.active[ids[j]] = 0;
-                        else keep = true;
+                        if (wl) {  // bench_from_list (_kernels.pyx:152-168)
+                            ids[j] = list_at(P, sm, p, dense, v, s);
+                            if (ids[j] <= cutoff) P.active[ids[j]] = 0;
+                            else keep = true;
+                        } else if (P.active[v]) {  // bench_sweep (_kernels.pyx:171-187)
+                            ids[j] = (int)v;
+                            if ((long long)v <= cutoff) P.active[v] = 0;
+                            else keep = true;
+                        }
                     }
                     bal[j] = __ballot_sync(FULL, keep);
                 }
