@@ -145,21 +145,22 @@ __global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
             for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * EPT) {
                 int ids[EPT];
                 unsigned bal[EPT];
+                // all EPT loads first (independent), then decide
 #pragma unroll
                 for (int j = 0; j < EPT; ++j) {
                     const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
-                    bool keep = false;
-                    ids[j] = 0;
+                    ids[j] = -1;
                     if (v < hi) {
-                        if (wl) {  // bench_from_list (_kernels.pyx:152-168)
-                            ids[j] = list_at(P, sm, p, dense, v, s);
-                            if (ids[j] <= cutoff) P.active[ids[j]] = 0;
-                            else keep = true;
-                        } else if (P.active[v]) {  // bench_sweep (_kernels.pyx:171-187)
-                            ids[j] = (int)v;
-                            if ((long long)v <= cutoff) P.active[v] = 0;
-                            else keep = true;
-                        }
+                        if (wl) ids[j] = list_at(P, sm, p, dense, v, s);     // bench_from_list
+                        else ids[j] = P.active[v] ? (int)v : -1;              // bench_sweep
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < EPT; ++j) {
+                    bool keep = false;
+                    if (ids[j] >= 0) {
+                        if (ids[j] <= cutoff) P.active[ids[j]] = 0;  // _kernels.pyx:159-160 / 178-179
+                        else keep = true;                            // push (_kernels.pyx:161-165)
                     }
                     bal[j] = __ballot_sync(FULL, keep);
                 }
