@@ -24,7 +24,7 @@ namespace pushbench {
 constexpr int BLOCK = 512;
 constexpr int NW = BLOCK / 32;
 constexpr int MAXG = 512;  // max CTAs (segments)
-constexpr int EPT = 16;    // elements per thread per tile
+constexpr int EPT = 8;     // elements per thread per tile
 static_assert(EPT * NW % 32 == 0, "scan layout");
 
 struct Ctrl {
@@ -60,7 +60,8 @@ __device__ __forceinline__ int list_at(const Params &P, const Smem &sm, int p, b
                                        unsigned &s) {
     if (dense) return (int)v;
     while (sm.prefix[s + 1] <= v) ++s;
-    return P.seg[p][(long long)s * P.segcap + (long long)(v - sm.prefix[s])];
+    const int *cur = p ? P.seg[1] : P.seg[0];  // select, not a runtime-indexed param array
+    return cur[(long long)s * P.segcap + (long long)(v - sm.prefix[s])];
 }
 
 __device__ __forceinline__ unsigned seg_of(const Smem &sm, unsigned nseg, unsigned long long v) {
@@ -92,7 +93,7 @@ __device__ __forceinline__ unsigned block_excl_sum(unsigned x, unsigned &total, 
     return r;
 }
 
-__global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
+__global__ void __launch_bounds__(BLOCK, 2) pushbench_kernel(Params P) {
     __shared__ Smem sm;
     Ctrl *C = P.ctrl;
     const unsigned G = P.nblocks;
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(BLOCK) pushbench_kernel(Params P) {
         // CTA shares rounded to 16 elements (aligned 16-byte flag loads)
         const unsigned long long lo = blockIdx.x == 0 ? 0 : ((span * blockIdx.x / G) & ~15ull);
         const unsigned long long hi = blockIdx.x + 1 == G ? span : ((span * (blockIdx.x + 1) / G) & ~15ull);
-        int *out = P.seg[np] + (long long)blockIdx.x * P.segcap;
+        int *out = (np ? P.seg[1] : P.seg[0]) + (long long)blockIdx.x * P.segcap;
         unsigned written = 0;
         {
             // element v = base + j*BLOCK + tid: coalesced reads of the flags

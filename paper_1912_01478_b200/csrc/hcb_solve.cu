@@ -157,6 +157,12 @@ struct Smem {
     unsigned out_cnt;
 };
 
+// dynamic list of parity p, bin b (selects instead of a runtime-indexed
+// kernel-parameter array, which would force a local-memory copy of Params)
+__device__ __forceinline__ int *dyn_list(const Params &P, int p, int b) {
+    return p ? P.dyn[1][b] : P.dyn[0][b];
+}
+
 __device__ __forceinline__ long long list_index(const List &L, const unsigned *prefix, unsigned long long v) {
     if (!L.segmented) return (long long)v;
     // last segment s with prefix[s] <= v (segments may be empty)
@@ -606,7 +612,7 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
     const unsigned csz = rc.csz[bin];
     const unsigned long long lo = (unsigned long long)c * csz;
     const unsigned long long hi = min(lo + csz, rc.L[bin].total);
-    int *out = P.dyn[np][bin] + (long long)c * csz;
+    int *out = dyn_list(P, np, bin) + (long long)c * csz;
     if (threadIdx.x == 0) sm.out_cnt = 0;
     __syncthreads();
     constexpr unsigned NG = 32 / G;
@@ -647,8 +653,8 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
                     my_conf += k;
                     if (STATS) my_edges[1] += low;
                     if (k) {
-                        if (is_hub) P.dyn[np][BIN_HUB][atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
-                        else P.dyn[np][3][c] = u;  // segment c, capacity 1
+                        if (is_hub) dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
+                        else dyn_list(P, np, 3)[c] = u;  // segment c, capacity 1
                         pushed = 1;
                     } else {
                         xput<F>(P, u, xu | FB<F>);
@@ -669,7 +675,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         const unsigned csz0 = rc.csz[0];
         const unsigned long long lo = (unsigned long long)c * csz0;
         const unsigned long long hi = min(lo + csz0, rc.L[0].total);
-        int *out = P.dyn[np][0] + (long long)c * csz0;
+        int *out = dyn_list(P, np, 0) + (long long)c * csz0;
         unsigned written = 0;
         for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
             int u[NPT];
@@ -776,10 +782,10 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         if (threadIdx.x == 0) {
             for (int b = 0; b < NSEG_BINS; ++b)
                 rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.nst[b], 0, 0, false}
-                                 : List{P.dyn[p][b], sm.prefix[b][rc.prev_nseg[b]], rc.prev_nseg[b],
+                                 : List{dyn_list(P, p, b), sm.prefix[b][rc.prev_nseg[b]], rc.prev_nseg[b],
                                         rc.prev_cap[b], true};
             const unsigned long long hub_total = t == 1 ? rc.nst[BIN_HUB] : ld_relaxed_u64(&C->hub_cnt[p]);
-            rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : P.dyn[p][BIN_HUB], hub_total, 0, 0, false};
+            rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : dyn_list(P, p, BIN_HUB), hub_total, 0, 0, false};
             unsigned long long s = 0;
             for (int b = 0; b < NBIN; ++b) s += rc.L[b].total;
             const bool topo = P.mode == HC_MODE_TOPO || (P.mode == HC_MODE_HYBRID && (long long)s > P.thr);
