@@ -165,6 +165,12 @@ __global__ void __launch_bounds__(BLOCK, 2) pushbench_kernel(Params P) {
                     }
                     bal[j] = __ballot_sync(FULL, keep);
                 }
+                // tiles without survivors (the deactivated prefix in push_nowl
+                // sweeps) skip the compaction: one barrier instead of three
+                unsigned any = 0;
+#pragma unroll
+                for (int j = 0; j < EPT; ++j) any |= bal[j];
+                if (!__syncthreads_or(any != 0)) continue;
                 if (lane < EPT) {
                     unsigned mine = 0;
 #pragma unroll
