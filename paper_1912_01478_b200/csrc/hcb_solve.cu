@@ -558,50 +558,6 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
     }
 }
 
-// Ordered compaction of a tile's losers (index order base + j*BLOCK + tid,
-// i.e. j-major then thread) into out[written ...]; returns the tile's count.
-__device__ __forceinline__ unsigned compact_tile(const int u[NPT], const bool lost[NPT], int *out,
-                                                 unsigned written, Smem &sm) {
-    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-    unsigned bal[NPT];
-#pragma unroll
-    for (int j = 0; j < NPT; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
-    if (lane < NPT) {
-        unsigned mine = 0;
-#pragma unroll
-        for (int j = 0; j < NPT; ++j)
-            if (lane == (unsigned)j) mine = __popc(bal[j]);
-        sm.warp_tmp[lane * NW + warp] = mine;
-    }
-    __syncthreads();
-    if (warp == 0) {  // scan the NPT*NW counts, CPL per lane
-        constexpr int CPL = (NPT * NW + 31) / 32;
-        unsigned a[CPL], sum = 0;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-            const unsigned i = CPL * lane + q;
-            a[q] = i < NPT * NW ? sm.warp_tmp[i] : 0u;
-            sum += a[q];
-        }
-        const unsigned incl = warp_incl_scan(sum);
-        unsigned run = incl - sum;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-            const unsigned i = CPL * lane + q;
-            if (i < NPT * NW) sm.warp_tmp[i] = run;
-            run += a[q];
-        }
-        if (lane == 31) sm.out_cnt = incl;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < NPT; ++j)
-        if (lost[j]) out[written + sm.warp_tmp[j * NW + warp] + __popc(bal[j] & lanemask_lt())] = u[j];
-    const unsigned tot = sm.out_cnt;
-    __syncthreads();
-    return tot;
-}
-
 // a chunk of a group bin: warps take warp tiles of 32/G nodes round-robin
 template <int G, typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Smem &sm, int bin,
@@ -676,14 +632,33 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         const unsigned long long lo = (unsigned long long)c * csz0;
         const unsigned long long hi = min(lo + csz0, rc.L[0].total);
         int *out = dyn_list(P, np, 0) + (long long)c * csz0;
-        unsigned written = 0;
+        // losers append warp by warp (runs of consecutive ids stay together;
+        // worklist order only affects locality, never results)
+        if (PHASE == 1) {
+            if (threadIdx.x == 0) sm.out_cnt = 0;
+            __syncthreads();
+        }
+        const unsigned lane = lane_id();
         for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
             int u[NPT];
             bool lost[NPT];
             small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
-            if (PHASE == 1) written += compact_tile(u, lost, out, written, sm);
+            if (PHASE == 1) {
+#pragma unroll
+                for (int j = 0; j < NPT; ++j) {
+                    const unsigned bal = __ballot_sync(FULL, lost[j]);
+                    if (!bal) continue;
+                    unsigned pos = 0;
+                    if (lane == 0) pos = atomicAdd(&sm.out_cnt, (unsigned)__popc(bal));
+                    pos = __shfl_sync(FULL, pos, 0);
+                    if (lost[j]) out[pos + __popc(bal & lanemask_lt())] = u[j];
+                }
+            }
         }
-        if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
+        if (PHASE == 1) {
+            __syncthreads();
+            if (threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = sm.out_cnt;
+        }
     }
 }
 
