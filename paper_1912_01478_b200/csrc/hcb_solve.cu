@@ -151,6 +151,7 @@ struct Smem {
     unsigned win_bm[NW][WIN_WORDS];
     unsigned hub_bm[HUB_WORDS];
     unsigned warp_tmp[NPT * NW];
+    unsigned cnt_tab[2][NPT * NW];
     unsigned long long red;
     int hub_first;
     unsigned unit;
@@ -632,33 +633,43 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         const unsigned long long lo = (unsigned long long)c * csz0;
         const unsigned long long hi = min(lo + csz0, rc.L[0].total);
         int *out = dyn_list(P, np, 0) + (long long)c * csz0;
-        // losers append warp by warp (runs of consecutive ids stay together;
-        // worklist order only affects locality, never results)
-        if (PHASE == 1) {
-            if (threadIdx.x == 0) sm.out_cnt = 0;
-            __syncthreads();
-        }
-        const unsigned lane = lane_id();
+        // order-preserving compaction of the losers (index order j-major, then
+        // thread), ONE barrier per tile: every warp publishes its per-j loser
+        // counts into a double-buffered table and scans it itself.  (Order only
+        // affects locality, but an unordered list fragments round after round.)
+        const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+        unsigned written = 0, buf = 0;
         for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
             int u[NPT];
             bool lost[NPT];
             small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
             if (PHASE == 1) {
+                unsigned bal[NPT];
+#pragma unroll
+                for (int j = 0; j < NPT; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
+                if (lane < NPT) {
+                    unsigned mine = 0;
+#pragma unroll
+                    for (int j = 0; j < NPT; ++j)
+                        if (lane == (unsigned)j) mine = __popc(bal[j]);
+                    sm.cnt_tab[buf][lane * NW + warp] = mine;
+                }
+                __syncthreads();
+                unsigned run = written;
 #pragma unroll
                 for (int j = 0; j < NPT; ++j) {
-                    const unsigned bal = __ballot_sync(FULL, lost[j]);
-                    if (!bal) continue;
-                    unsigned pos = 0;
-                    if (lane == 0) pos = atomicAdd(&sm.out_cnt, (unsigned)__popc(bal));
-                    pos = __shfl_sync(FULL, pos, 0);
-                    if (lost[j]) out[pos + __popc(bal & lanemask_lt())] = u[j];
+                    const unsigned v = lane < NW ? sm.cnt_tab[buf][j * NW + lane] : 0u;
+                    const unsigned incl = warp_incl_scan(v);
+                    const unsigned before = __shfl_sync(FULL, incl - v, warp);  // warps < me in slice j
+                    const unsigned tot_j = __shfl_sync(FULL, incl, 31);
+                    if (lost[j]) out[run + before + __popc(bal[j] & lanemask_lt())] = u[j];
+                    run += tot_j;
                 }
+                written = run;
+                buf ^= 1u;
             }
         }
-        if (PHASE == 1) {
-            __syncthreads();
-            if (threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = sm.out_cnt;
-        }
+        if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
     }
 }
 
