@@ -106,6 +106,17 @@ struct Ctrl {
     unsigned segcnt[2][NSEG_BINS][MAXSEG];       // [parity][bin][segment] loser counts
 };
 
+// per-hub merge slot for hubs split across several CTAs (latency regime)
+constexpr int HA_WORDS = 62;                   // colors 65..2048 beyond the 64-bit mask
+constexpr int MAX_SPLIT_SLOTS = 1024;
+struct HubAcc {
+    unsigned long long mask;                   // colors 1..64 seen (assign)
+    unsigned words[HA_WORDS];                  // colors 65..2048 seen (assign)
+    unsigned cnt, low;                         // conflicts / lower neighbours (resolve)
+    unsigned arrive;                           // slices done
+    unsigned pad;
+};
+
 struct Params {
     const void *ro;            // int32 or int64 row offsets (template OffT)
     const int *ci;
@@ -122,6 +133,7 @@ struct Params {
     long long thr;
     unsigned nblocks;
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
+    HubAcc *hub_acc;           // MAX_SPLIT_SLOTS merge slots (zeroed; reset by their last slice)
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -142,6 +154,7 @@ struct RoundCfg {
     unsigned csz[NSEG_BINS], nch[NSEG_BINS];
     unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
     unsigned prev_nseg[NSEG_BINS], prev_cap[NSEG_BINS];
+    unsigned hub_k;                // CTAs per hub (>1: hubs split, latency regime)
     bool topo, ident, bin3_by_cta, ident_small;
 };
 
@@ -580,6 +593,132 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
     if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][bin][c] = sm.out_cnt;
 }
 
+// ------------------------------------------------------------------ split hubs
+// Slice `slice` of k of hub u's adjacency, one CTA.  Partial results merge
+// into the hub's global slot; the last slice to arrive finalizes (mex /
+// winner-loser decision) and resets the slot for the next round.
+template <typename OffT, class F>
+__device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigned slice, unsigned k,
+                                 HubAcc &acc, Smem &sm, bool &last) {
+    const long long b0 = ro[u], e0 = ro[u + 1], len = e0 - b0;
+    const long long b = b0 + len * slice / k, e = b0 + len * (slice + 1) / k;
+    for (int i = threadIdx.x; i < HA_WORDS + 2; i += BLOCK) sm.hub_bm[i] = 0u;  // [0,1]: mask, [2..]: words
+    __syncthreads();
+    unsigned long long mask = 0;
+    for (long long kk = b + threadIdx.x; kk < e; kk += 4 * BLOCK) {
+        int v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = (kk + q * BLOCK < e) ? colget<F>(P, kk + q * BLOCK, u) : -1;
+        unsigned x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned c = x[q] & CM<F>;
+            if (!(x[q] & FB<F>)) continue;
+            if (c <= 64u) mask |= 1ull << (c - 1u);
+            else if (c <= 64u + 32u * HA_WORDS) mark(sm.hub_bm + 2, c - 64u);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mask |= __shfl_xor_sync(FULL, mask, o);
+    if (lane_id() == 0 && mask) {
+        atomicOr(&sm.hub_bm[0], (unsigned)mask);
+        atomicOr(&sm.hub_bm[1], (unsigned)(mask >> 32));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned long long m = (unsigned long long)sm.hub_bm[0] | ((unsigned long long)sm.hub_bm[1] << 32);
+        if (m) atomicOr(&acc.mask, m);
+    }
+    for (int i = threadIdx.x; i < HA_WORDS; i += BLOCK)
+        if (sm.hub_bm[2 + i]) atomicOr(&acc.words[i], sm.hub_bm[2 + i]);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        sm.hub_first = atomicAdd(&acc.arrive, 1u) == k - 1 ? 1 : 0;
+    }
+    __syncthreads();
+    last = sm.hub_first == 1;
+    unsigned T = 0;
+    if (last) {  // CTA-uniform
+        __threadfence();
+        if (threadIdx.x == 0) {
+            const unsigned long long m = __ldcg(&acc.mask);
+            if (m != ~0ull) {
+                T = (unsigned)__ffsll((long long)~m);
+            } else {
+                for (int i = 0; i < HA_WORDS && !T; ++i) {
+                    const unsigned w = __ldcg(&acc.words[i]);
+                    if (w != FULL) T = 64u + 32u * i + (unsigned)__ffs(~w);
+                }
+            }
+            sm.hub_first = (int)T;  // 0: every color <= 2048 taken
+            acc.mask = 0;
+            for (int i = 0; i < HA_WORDS; ++i) acc.words[i] = 0;
+            acc.arrive = 0;
+        }
+        __syncthreads();
+        T = (unsigned)sm.hub_first;
+        __syncthreads();
+        if (T == 0) T = assign_cta<OffT, F>(P, ro, u, sm);  // exact full scan (colors > 2048)
+    }
+    return T;
+}
+
+template <typename OffT, class F>
+__device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsigned T, unsigned slice, unsigned k,
+                                  HubAcc &acc, Smem &sm, bool &last, unsigned &low_out) {
+    const long long b0 = ro[u], e0 = ro[u + 1], len = e0 - b0;
+    const long long b = b0 + len * slice / k, e = b0 + len * (slice + 1) / k;
+    const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+    unsigned cnt = 0, low = 0;
+    for (long long k0 = b + (long long)warp * 128; k0 < e; k0 += 128LL * NW) {
+        int v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const long long kk = k0 + 32 * q + lane;
+            v[q] = kk < e ? colget<F>(P, kk, u) : 0x7fffffff;
+        }
+        unsigned x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
+        bool stop = false;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
+            else stop = true;
+        }
+        if (__any_sync(FULL, stop)) break;  // adjacency sorted: the rest is >= u
+    }
+    cnt = warp_sum(cnt);
+    low = warp_sum(low);
+    if (lane == 0 && (cnt | low)) {
+        atomicAdd(&acc.cnt, cnt);
+        atomicAdd(&acc.low, low);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        sm.hub_first = atomicAdd(&acc.arrive, 1u) == k - 1 ? 1 : 0;
+    }
+    __syncthreads();
+    last = sm.hub_first == 1;
+    unsigned total = 0;
+    if (last) {
+        __threadfence();
+        total = __ldcg(&acc.cnt);
+        low_out = __ldcg(&acc.low);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            acc.cnt = 0;
+            acc.low = 0;
+            acc.arrive = 0;
+        }
+    }
+    return total;
+}
+
 // One unit of one phase.  All CTA-uniform inputs come from shared memory.
 // Unit ranges: [ubase0, ubase1) hubs, then bins 3, 2, 1, 0.
 template <typename OffT, class F, bool STATS, int PHASE>
@@ -590,6 +729,32 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
     const int np = p ^ 1;
     const unsigned *ub = rc.ubase;
     const bool is_hub = unit < ub[1];
+    if (is_hub && rc.hub_k > 1) {
+        // ---- hub split across hub_k CTAs (few active hubs: latency regime)
+        const unsigned k = rc.hub_k, slot = unit / k, slice = unit % k;
+        const int u = rc.L[BIN_HUB].base[slot];
+        const unsigned xu = xget<F>(P, u);
+        if (rc.topo && (xu & FB<F>)) return;  // topology sweep: inactive (_kernels.pyx:76)
+        HubAcc &acc = P.hub_acc[slot];
+        bool last;
+        if (PHASE == 0) {
+            const unsigned T = assign_slice<OffT, F>(P, ro, u, slice, k, acc, sm, last);
+            if (last && threadIdx.x == 0) {
+                xput<F>(P, u, T);
+                if (STATS) my_edges[0] += ro[u + 1] - ro[u];
+            }
+        } else {
+            unsigned low = 0;
+            const unsigned kc = resolve_slice<OffT, F>(P, ro, u, xu, slice, k, acc, sm, last, low);
+            if (last && threadIdx.x == 0) {
+                my_conf += kc;
+                if (STATS) my_edges[1] += low;
+                if (kc) dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
+                else xput<F>(P, u, xu | FB<F>);
+            }
+        }
+        return;
+    }
     if (is_hub || (rc.bin3_by_cta && unit < ub[2])) {
         // ---- hub (or bin-3 node in the latency regime): one CTA per node
         const unsigned c = is_hub ? unit : unit - ub[1];
@@ -790,7 +955,10 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
             rc.bin3_by_cta = rc.csz[3] == 1u;
             const bool live = s != 0;
             rc.ubase[0] = 0;
-            rc.ubase[1] = live ? (unsigned)rc.L[BIN_HUB].total : 0u;
+            // few active hubs: split each across nblocks/H CTAs (<= MAX_SPLIT_SLOTS hubs)
+            const unsigned H = (unsigned)rc.L[BIN_HUB].total;
+            rc.hub_k = (H > 0 && H < P.nblocks / 2 && H <= MAX_SPLIT_SLOTS) ? P.nblocks / H : 1u;
+            rc.ubase[1] = live ? H * rc.hub_k : 0u;
             rc.ubase[2] = rc.ubase[1] + (live ? rc.nch[3] : 0u);
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
             rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
@@ -923,7 +1091,7 @@ inline size_t seg_capacity(long long cnt) {
 }
 
 struct Layout {
-    size_t x, stat, dyn[2][NBIN], ro32, ci16, ctrl, part, total;
+    size_t x, stat, dyn[2][NBIN], ro32, ci16, hub_acc, ctrl, part, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
@@ -940,6 +1108,7 @@ static Layout layout(long long n, long long m) {
         }
     L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
     L.ci16 = o; o = align_up(o + (m < 0x7fffffffLL ? 2 * (size_t)m : 0) + 256, 256);
+    L.hub_acc = o; o = align_up(o + sizeof(HubAcc) * MAX_SPLIT_SLOTS, 256);
     L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
     L.part = o; o = align_up(o + part_scratch_bytes(NKEY, n), 256);
     L.total = o;
@@ -1050,6 +1219,8 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
         HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
 
     HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
+    P.hub_acc = reinterpret_cast<HubAcc *>(ws + L.hub_acc);
+    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
     const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
     // static degree-bucketed lists (bins contiguous, see DegreeKey)
     unsigned long long *totals = nullptr;
