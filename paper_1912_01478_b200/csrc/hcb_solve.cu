@@ -103,6 +103,8 @@ struct Ctrl {
     unsigned int unit_ctr[2][2];                 // [phase][parity]
     long long rounds;
     long long rec_overflow;
+    unsigned fmt_overflow;                       // a tentative color exceeded the state word
+    unsigned pad1;
     unsigned segcnt[2][NSEG_BINS][MAXSEG];       // [parity][bin][segment] loser counts
 };
 
@@ -134,6 +136,7 @@ struct Params {
     unsigned nblocks;
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
     HubAcc *hub_acc;           // MAX_SPLIT_SLOTS merge slots (zeroed; reset by their last slice)
+    unsigned *fmt_overflow;    // set when a tentative color does not fit the state word
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -154,12 +157,14 @@ struct RoundCfg {
     unsigned csz[NSEG_BINS], nch[NSEG_BINS];
     unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
     unsigned prev_nseg[NSEG_BINS], prev_cap[NSEG_BINS];
-    unsigned hub_k;                // CTAs per hub (>1: hubs split, latency regime)
+    unsigned hub_split;            // hubs split into equal-size edge slices (latency regime)
+    unsigned hub_slice;            // edges per slice
     bool topo, ident, bin3_by_cta, ident_small;
 };
 
 struct Smem {
     RoundCfg rc;
+    unsigned hub_pre[MAX_SPLIT_SLOTS + 1];    // slice prefix over the active hubs (split rounds)
     unsigned prefix[NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
     unsigned win_bm[NW][WIN_WORDS];
     unsigned hub_bm[HUB_WORDS];
@@ -251,6 +256,13 @@ __device__ __forceinline__ unsigned xget(const Params &P, long long v) {
 template <class F>
 __device__ __forceinline__ void xput(const Params &P, long long v, unsigned w) {
     reinterpret_cast<typename F::xt *>(P.X)[v] = (typename F::xt)w;
+}
+// tentative color write: a 16-bit word cannot hold T > 32767 (possible only
+// for degree > 32766); flag it, the host reruns the solve with 32-bit words
+template <class F>
+__device__ __forceinline__ void xput_t(const Params &P, long long v, unsigned T) {
+    if (sizeof(typename F::xt) == 2 && T > CM<F>) *P.fmt_overflow = 1u;
+    xput<F>(P, v, T);
 }
 // streaming load of a column id (evict-first so the X gathers keep L2)
 template <class F>
@@ -729,9 +741,15 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
     const int np = p ^ 1;
     const unsigned *ub = rc.ubase;
     const bool is_hub = unit < ub[1];
-    if (is_hub && rc.hub_k > 1) {
-        // ---- hub split across hub_k CTAs (few active hubs: latency regime)
-        const unsigned k = rc.hub_k, slot = unit / k, slice = unit % k;
+    if (is_hub && rc.hub_split) {
+        // ---- hub split into equal-size edge slices (few active hubs)
+        unsigned lo = 0, hi = rc.L[BIN_HUB].total;  // hub with hub_pre[i] <= unit < hub_pre[i+1]
+        while (hi - lo > 1) {
+            const unsigned mid = (lo + hi) >> 1;
+            if (sm.hub_pre[mid] <= unit) lo = mid;
+            else hi = mid;
+        }
+        const unsigned slot = lo, slice = unit - sm.hub_pre[lo], k = sm.hub_pre[lo + 1] - sm.hub_pre[lo];
         const int u = rc.L[BIN_HUB].base[slot];
         const unsigned xu = xget<F>(P, u);
         if (rc.topo && (xu & FB<F>)) return;  // topology sweep: inactive (_kernels.pyx:76)
@@ -740,7 +758,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
         if (PHASE == 0) {
             const unsigned T = assign_slice<OffT, F>(P, ro, u, slice, k, acc, sm, last);
             if (last && threadIdx.x == 0) {
-                xput<F>(P, u, T);
+                xput_t<F>(P, u, T);
                 if (STATS) my_edges[0] += ro[u + 1] - ro[u];
             }
         } else {
@@ -765,7 +783,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
             if (PHASE == 0) {
                 const unsigned T = assign_cta<OffT, F>(P, ro, u, sm);
                 if (threadIdx.x == 0) {
-                    xput<F>(P, u, T);
+                    xput_t<F>(P, u, T);
                     if (STATS) my_edges[0] += ro[u + 1] - ro[u];
                 }
             } else {
@@ -955,10 +973,11 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
             rc.bin3_by_cta = rc.csz[3] == 1u;
             const bool live = s != 0;
             rc.ubase[0] = 0;
-            // few active hubs: split each across nblocks/H CTAs (<= MAX_SPLIT_SLOTS hubs)
+            // few active hubs (< nblocks): split them into edge slices; the
+            // slice prefix is built below by the whole CTA
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
-            rc.hub_k = (H > 0 && H < P.nblocks / 2 && H <= MAX_SPLIT_SLOTS) ? P.nblocks / H : 1u;
-            rc.ubase[1] = live ? H * rc.hub_k : 0u;
+            rc.hub_split = (live && H > 0 && H < P.nblocks && H <= MAX_SPLIT_SLOTS) ? 1u : 0u;
+            rc.ubase[1] = live ? H : 0u;
             rc.ubase[2] = rc.ubase[1] + (live ? rc.nch[3] : 0u);
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
             rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
@@ -991,6 +1010,34 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         const unsigned long long s = sm.red;
         __syncthreads();
         if (s == 0) break;  // worklist drained (driver.py:145)
+        if (rc.hub_split) {  // CTA-uniform: equal-size edge slices over the active hubs
+            const unsigned H = (unsigned)rc.L[BIN_HUB].total;
+            unsigned long long e_loc = 0;
+            for (unsigned i = threadIdx.x; i < H; i += BLOCK) {
+                const int u = rc.L[BIN_HUB].base[i];
+                e_loc += (unsigned long long)(ro[u + 1] - ro[u]);
+            }
+            e_loc = warp_sum(e_loc);
+            if (threadIdx.x == 0) sm.red = 0;
+            __syncthreads();
+            if (lane == 0 && e_loc) atomicAdd(&sm.red, e_loc);
+            __syncthreads();
+            // ~2 slices per CTA in total, at least 4096 edges each
+            const unsigned long long S = max(4096ull, (sm.red + 2ull * P.nblocks - 1) / (2ull * P.nblocks));
+            for (unsigned i = threadIdx.x; i < H; i += BLOCK) {
+                const int u = rc.L[BIN_HUB].base[i];
+                const unsigned long long d = (unsigned long long)(ro[u + 1] - ro[u]);
+                sm.hub_pre[i + 1] = (unsigned)max(1ull, (d + S - 1) / S);
+            }
+            if (threadIdx.x == 0) sm.hub_pre[0] = 0;
+            __syncthreads();
+            if (threadIdx.x == 0) {  // H < nblocks <= a few hundred: serial scan
+                for (unsigned i = 1; i <= H; ++i) sm.hub_pre[i] += sm.hub_pre[i - 1];
+                const unsigned extra = sm.hub_pre[H] - H;
+                for (int b = 1; b <= NBIN; ++b) rc.ubase[b] += extra;
+            }
+            __syncthreads();
+        }
 
         run_phase<OffT, F, STATS, 0>(P, ro, sm, p, my_conf, my_edges);
         grid_sync(&C->bar, P.nblocks);
@@ -1251,17 +1298,35 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     HC_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
-    const bool x16 = (HC_FMT16 != 0) && !g_no_x16 && h_tot[9] + h_tot[10] + h_tot[11] + h_tot[12] == 0;
+    // 16-bit words are exact when max degree <= 16384 (mex <= 16385); above
+    // that they are used speculatively and the solve is redone with 32-bit
+    // words if any tentative color overflows (never for the BASELINE graphs)
+    const bool x16_exact = h_tot[9] + h_tot[10] + h_tot[11] + h_tot[12] == 0;
+    bool x16 = (HC_FMT16 != 0) && !g_no_x16;
     const bool c16 = (HC_FMT16 != 0) && !g_no_c16 && narrow && num_edges > 0 && h_bad == 0;
     const int per_sm = occupancy();
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * sms);
-    void *args[] = {&P};
-    const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr);
-    HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
-    long long info[2];
-    HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
-    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    P.fmt_overflow = &P.ctrl->fmt_overflow;
+    long long info[3];
+    for (int attempt = 0;; ++attempt) {
+        if (attempt > 0) {  // fresh control block (keeps nstat via copy_totals)
+            HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
+            copy_totals_kernel<<<1, 32, 0, st>>>(totals, P.ctrl);
+            HC_CHECK_LAUNCH();
+            HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
+            if (d_stats && P.max_rec)
+                HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
+        }
+        void *args[] = {&P};
+        const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr);
+        HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
+        HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
+        HC_CUDA_TRY(cudaStreamSynchronize(st));
+        const unsigned overflow = (unsigned)(info[2] & 0xffffffffLL);
+        if (!(x16 && overflow) || x16_exact) break;
+        x16 = false;  // redo with 32-bit state words
+    }
     if (h_rounds) *h_rounds = info[0];
     HC_REQUIRE(!info[1], HC_ERR_RECORDS, "hc_solve: %lld rounds exceed the %lld-record buffer",
                info[0], (long long)max_rec);
