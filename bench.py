@@ -150,20 +150,21 @@ def host_csr(cfg):
     return n, ro, ci
 
 
-def cpu_sample(ref, g, budget_s: float, full_visits: int | None):
+def cpu_sample(ref, g, budget_s: float, work: list | None):
     """Run the reference's hybrid loop (driver.py:143-169, through its public
     data_driven_iteration / topology_driven_iteration) on the host for at most
     `budget_s` seconds.  If the solve finishes, the rate is exact; otherwise the
-    full-solve time is extrapolated from the node-visit rate of the sampled
-    rounds: T_full = T_sample * sum_t|W_t| (whole solve, known from the
-    bit-identical GPU trajectory) / sum_{t<=R}|W_t| (sampled)."""
+    full-solve time is extrapolated from the sampled rounds by per-round work
+    (node visits + edge visits of round t, known exactly from the
+    bit-identical GPU trajectory, hc_solve_stats):
+        T_full = T_sample * sum_t work_t / sum_{t<=R} work_t."""
     workers = os.cpu_count() or 1
     cfgr = ref.HybridConfig(mode="hybrid", workers=workers)
     n = g.num_nodes
     thr = math.ceil(cfgr.threshold_fraction * n)
     state = ref.ColorState.fresh(n)
     wl = ref.Worklist.init_full(n)
-    round_no, visits, t_loop = 1, 0, 0.0
+    round_no, t_loop = 1, 0.0
     t0 = time.perf_counter()
     while len(wl.current) > 0:
         size_in = len(wl.current)
@@ -171,20 +172,22 @@ def cpu_sample(ref, g, budget_s: float, full_visits: int | None):
         ts = time.perf_counter()
         it(g, state, wl, round_no, workers=workers, chunk_size=cfgr.chunk_size)
         t_loop += time.perf_counter() - ts
-        visits += size_in
         round_no += 1
         if time.perf_counter() - t0 > budget_s:
             break
+    rounds = round_no - 1
     finished = len(wl.current) == 0
     if finished:
         secs = t_loop
-        sample = f"full hybrid solve ({round_no - 1} rounds)"
+        sample = f"full hybrid solve ({rounds} rounds)"
     else:
-        if not full_visits:
+        if not work:
             return None
-        secs = t_loop * full_visits / visits
-        sample = (f"first {round_no - 1} rounds of the hybrid solve ({visits} of {full_visits} node-visits), "
-                  f"extrapolated by node-visit rate")
+        done = float(sum(work[:rounds]))
+        total = float(sum(work))
+        secs = t_loop * total / done
+        sample = (f"first {rounds} of {len(work)} rounds of the hybrid solve ({100 * done / total:.2f}% of the "
+                  f"node+edge visits), extrapolated by per-round work")
     return {"value": (g.num_edges // 2) / secs, "unit": UNIT, "cores": workers, "kind": "reference",
             "sample": sample, "solve_seconds": secs, "finished": finished}
 
@@ -212,15 +215,15 @@ def run_reference(args, cfg):
     warm_reference(ref)
     n, ro, ci = host_csr(cfg)
     g = ref.CsrGraph(n, len(ci), ro, ci)
-    full_visits = known_visits(args.config)
+    work = known_work(args.config)
     steps = max(1, args.steps)
     per_step = min(30.0, max(5.0, 150.0 / (steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_sample(ref, g, per_step / 3, full_visits)
+        cpu_sample(ref, g, per_step / 3, work)
     vals = []
     last = None
     for _ in range(steps):
-        last = cpu_sample(ref, g, per_step, full_visits)
+        last = cpu_sample(ref, g, per_step, work)
         vals.append(last["value"])
     value = float(statistics.mean(vals))
     line = {
@@ -238,14 +241,19 @@ def run_reference(args, cfg):
     return 0
 
 
-def known_visits(config):
-    """sum_t |W_t| of the full solve, for configs whose trajectory is known in
-    closed form (grid: the wavefront colors the anti-diagonals; measured on
-    the GPU and pinned by tests) -- else None (filled in from the GPU run)."""
-    p = REPO / "profiles" / f"visits_{config}.json"
+def known_work(config):
+    """Per-round work (node + edge visits) of the full hybrid solve, recorded
+    from the bit-identical GPU trajectory (profiles/work_<config>.json, written
+    by scripts/work_profile.py) -- the reference arm runs without a GPU."""
+    p = REPO / "profiles" / f"work_{config}.json"
     if p.exists():
-        return json.loads(p.read_text())["sum_wl_in"]
+        return json.loads(p.read_text())["work"]
     return None
+
+
+def round_work(records, stats):
+    """node visits + edge visits per round (assign edges + resolve lower edges)."""
+    return [int(r[2]) + int(a) + int(b) for r, (a, b) in zip(records, stats)]
 
 
 # --------------------------------------------------------------------------
@@ -467,7 +475,7 @@ def run_ours(args, cfg):
             ref = reference_module()
             warm_reference(ref)
             g = ref.CsrGraph(host.num_nodes, host.num_edges, host.row_offsets, host.col_indices)
-            line["cpu_baseline"] = cpu_sample(ref, g, args.cpu_budget, sum_visits)
+            line["cpu_baseline"] = cpu_sample(ref, g, args.cpu_budget, round_work(recs, st))
         except Exception as exc:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "unavailable": repr(exc)}
     if rank == 0:
