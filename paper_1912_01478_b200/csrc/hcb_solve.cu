@@ -264,13 +264,15 @@ __device__ __forceinline__ void xput_t(const Params &P, long long v, unsigned T)
     if (sizeof(typename F::xt) == 2 && T > CM<F>) *P.fmt_overflow = 1u;
     xput<F>(P, v, T);
 }
-// streaming load of a column id (evict-first so the X gathers keep L2)
-template <class F>
+// load of a column id.  Low-degree rows are streamed (evict-first, so the
+// X gathers keep L2); hub / bin-3 rows (KEEP) are cached at L2 normally:
+// the same hub adjacency is re-scanned in every round of the hub core.
+template <class F, bool KEEP = false>
 __device__ __forceinline__ int colget(const Params &P, long long k, int u) {
     if constexpr (sizeof(typename F::ct) == 4)
-        return __ldcs(P.ci + k);
+        return KEEP ? __ldcg(P.ci + k) : __ldcs(P.ci + k);
     else
-        return u + (int)__ldcs(P.ci16 + k);
+        return u + (int)(KEEP ? __ldcg(P.ci16 + k) : __ldcs(P.ci16 + k));
 }
 
 template <class F>
@@ -419,7 +421,7 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
         for (long long k = b + threadIdx.x; k < e; k += 4 * BLOCK) {
             int v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? colget<F>(P, k + q * BLOCK, u) : -1;
+            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? colget<F, true>(P, k + q * BLOCK, u) : -1;
             unsigned x[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
@@ -456,7 +458,7 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long k = k0 + 32 * q + lane;
-            v[q] = k < e ? colget<F>(P, k, u) : 0x7fffffff;
+            v[q] = k < e ? colget<F, true>(P, k, u) : 0x7fffffff;
         }
         unsigned x[4];
 #pragma unroll
@@ -620,7 +622,7 @@ __device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigne
     for (long long kk = b + threadIdx.x; kk < e; kk += 4 * BLOCK) {
         int v[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = (kk + q * BLOCK < e) ? colget<F>(P, kk + q * BLOCK, u) : -1;
+        for (int q = 0; q < 4; ++q) v[q] = (kk + q * BLOCK < e) ? colget<F, true>(P, kk + q * BLOCK, u) : -1;
         unsigned x[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
@@ -690,7 +692,7 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long kk = k0 + 32 * q + lane;
-            v[q] = kk < e ? colget<F>(P, kk, u) : 0x7fffffff;
+            v[q] = kk < e ? colget<F, true>(P, kk, u) : 0x7fffffff;
         }
         unsigned x[4];
 #pragma unroll
