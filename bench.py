@@ -348,17 +348,12 @@ def run_ours(args, cfg):
     import ctypes
 
     import torch
-    import torch.distributed as dist
 
     import paper_1912_01478_b200 as hc
     from paper_1912_01478_b200 import _lib
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = 1, 0, int(os.environ.get("LOCAL_RANK", "0"))  # N > 1: run_distributed
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     dg = build_graph(hc, cfg)
@@ -390,8 +385,6 @@ def run_ours(args, cfg):
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stream = torch.cuda.current_stream()
     launches_per_step = 6  # bucket count/scan/scatter + copy_totals + narrow_offsets + solve_kernel
-    if world > 1:
-        dist.barrier()
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         for i in range(args.steps):
@@ -404,14 +397,8 @@ def run_ours(args, cfg):
             stops[i].record(stream)
             _lib.check(rc)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
     total_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = world * und * args.steps / (total_ms / 1e3)
     clocks = clk.summary()
@@ -441,10 +428,6 @@ def run_ours(args, cfg):
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         assert rep.valid
     e2e_total = float(sum(e2e_ms))
-    if world > 1:
-        t = torch.tensor([e2e_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
     e2e_value = world * und * args.steps / (e2e_total / 1e3)
 
     hbm, peak_kind = peaks()
@@ -457,7 +440,7 @@ def run_ours(args, cfg):
         "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": args.mode,
                    "num_nodes": n, "num_undirected_edges": und, "rounds": R,
                    "sum_wl_in": sum_visits, "l2": "flushed between timed steps (512 MiB write)",
-                   "parallelism": "replicas" if world > 1 else "single-gpu"},
+                   "parallelism": "single-gpu"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
                      "kernel": "solve_kernel (+ bin preprocessing, whole hc_solve step)",
@@ -470,7 +453,7 @@ def run_ours(args, cfg):
                 "d2h_bytes_per_step": 8 * n + 48 * R, "ms_per_step": e2e_total / args.steps},
         "step_ms": step_ms,
     }
-    if rank == 0 and world == 1 and not args.skip_cpu:
+    if not args.skip_cpu:
         try:
             ref = reference_module()
             warm_reference(ref)
@@ -478,10 +461,7 @@ def run_ours(args, cfg):
             line["cpu_baseline"] = cpu_sample(ref, g, args.cpu_budget, round_work(recs, st))
         except Exception as exc:  # reported, not fatal
             line["cpu_baseline"] = {"value": None, "unavailable": repr(exc)}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
     return 0
 
 
