@@ -1,0 +1,30 @@
+"""Small workloads for compute-sanitizer (memcheck / synccheck / racecheck)."""
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np
+
+import paper_1912_01478_b200 as hc
+from oracle import oracle as O
+from paper_1912_01478_b200.pushbench import BenchConfig, run_push_bench
+
+for scale in (8, 10):
+    dg = hc.rmat_graph(scale, 16, 1)
+    ro, ci = O.build_csr(1 << scale, O.gen_rmat(scale, 16, 1))
+    for mode in ("data", "topo", "hybrid"):
+        c, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+        want, _ = O.color(ro, ci, mode)
+        assert np.array_equal(c, want)
+dg = hc.grid_graph(40, 30)
+c, rep = hc.color_graph(dg)
+# star hub (bin 4, split slices) + per-round plugin API + worklist sort
+n = 6000
+e = np.concatenate([np.column_stack([np.zeros(n - 1, np.int64), np.arange(1, n)]),
+                    np.random.default_rng(1).integers(0, n, (3000, 2))])
+g = hc.build_csr(hc.EdgeList(n, e))
+c, rep = hc.color_graph(g)
+state, wl = hc.ColorState.fresh(n), hc.Worklist.init_full(n)
+hc.data_driven_iteration(g, state, wl, 1)
+hc.topology_driven_iteration(g, state, wl, 2)
+run_push_bench(5000, BenchConfig(batch_size=300, repetitions=1))
+print("sanitize workload ok")
