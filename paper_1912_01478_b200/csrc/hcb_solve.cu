@@ -654,6 +654,7 @@ __device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigne
     }
     __syncthreads();
     last = sm.hub_first == 1;
+    __syncthreads();  // every thread has read the flag before thread 0 reuses it
     unsigned T = 0;
     if (last) {  // CTA-uniform
         __threadfence();
@@ -718,6 +719,7 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
     }
     __syncthreads();
     last = sm.hub_first == 1;
+    __syncthreads();
     unsigned total = 0;
     if (last) {
         __threadfence();
