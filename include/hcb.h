@@ -39,6 +39,7 @@ extern "C" {
 #define HC_ERR_UNCOLORED (-5)    /* colors_used on a 0 entry: driver.py:183-184         */
 #define HC_ERR_DUPLICATE (-6)    /* duplicate push in one iteration: worklist.py:85-88  */
 #define HC_ERR_RECORDS (-7)      /* per-round record buffer too small (rounds returned) */
+#define HC_ERR_TIMEOUT (-8)      /* multi-GPU: a peer missed a cross-GPU barrier       */
 
 #define HC_MODE_DATA 0   /* driver.py:149-150 */
 #define HC_MODE_TOPO 1   /* driver.py:147-148 */
@@ -142,6 +143,44 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
                    int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
                    hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, int64_t *d_stats,
                    void *d_ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------ */
+/* Device-resident multi-GPU solve over NVLink peer memory (SURVEY.md   */
+/* §8(e); replaces driver.py:122-176 on a 1D vertex partition).  One    */
+/* process (or one stream) per rank; rank r owns nodes [lo, hi) and     */
+/* runs ONE persistent kernel for the whole solve.  Every rank has a    */
+/* "shared region" (hc_mg_shared_bytes, zero-initialised once by the    */
+/* caller) holding its replica of the state words plus a mailbox; all   */
+/* ranks' regions are mapped into every rank (hc_mg_ipc_* between       */
+/* processes, plain pointers within one).  Owned boundary words are     */
+/* stored straight into every peer's replica (NVLink stores), and the   */
+/* per-round grid barriers are cross-GPU barriers that also all-reduce  */
+/* (|W'|, conflicts) for the identical hybrid decision on every rank    */
+/* (driver.py:145-152).  Colors, rounds and per-round records are       */
+/* bit-identical to hc_solve for every partition.                       */
+/*   hc_mg_solve: preprocessing (synchronous) + launch (asynchronous);  */
+/*     d_colors int64[hi-lo] receives the owned colors; every rank's    */
+/*     d_rec gets the same global records; ctas = 0: all resident CTAs; */
+/*     timeout_ms bounds each cross-GPU wait (<= 0: 60 s).  ctas > 0:   */
+/*     the caller sizes the grid (several ranks sharing one GPU, e.g.   */
+/*     tests) and guarantees co-residency; it is a regular launch.      */
+/*   hc_mg_wait: synchronises the stream, *h_rounds = rounds; returns   */
+/*     HC_ERR_TIMEOUT if a peer missed a barrier (the shared regions    */
+/*     must then be re-zeroed on every rank before the next solve).     */
+/* ------------------------------------------------------------------ */
+#define HC_IPC_HANDLE_BYTES 64
+size_t hc_mg_shared_bytes(int64_t num_nodes);
+size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t num_edges, int64_t lo, int64_t hi);
+/* export a device pointer for another process: cudaIpc handle of the
+ * allocation that contains it + the pointer's offset in it */
+int hc_mg_ipc_export(const void *d_ptr, void *h_handle, int64_t *h_offset);
+int hc_mg_ipc_import(const void *h_handle, int64_t offset, void **h_dptr);
+int hc_mg_ipc_close(void *d_ptr, int64_t offset);
+int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
+int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream);
 
 /* ------------------------------------------------------------------ */
 /* 1D-partitioned multi-GPU solve: per-phase kernels  */

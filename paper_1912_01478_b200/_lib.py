@@ -26,6 +26,7 @@ HC_ERR_WORKSPACE = -4
 HC_ERR_UNCOLORED = -5
 HC_ERR_DUPLICATE = -6
 HC_ERR_RECORDS = -7
+HC_ERR_TIMEOUT = -8
 
 MODE_CODES = {"data": 0, "topo": 1, "hybrid": 2}
 
@@ -75,6 +76,14 @@ _SIGS = {
     "hc_solve_set_formats": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "hc_solve": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_stats": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, _p, ctypes.c_size_t, _p]),
+    "hc_mg_shared_bytes": (ctypes.c_size_t, [_i64]),
+    "hc_mg_workspace_bytes": (ctypes.c_size_t, [_i64, _i64, _i64, _i64]),
+    "hc_mg_ipc_export": (ctypes.c_int, [_p, _p, _p]),
+    "hc_mg_ipc_import": (ctypes.c_int, [_p, _i64, _p]),
+    "hc_mg_ipc_close": (ctypes.c_int, [_p, _i64]),
+    "hc_mg_solve": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
+                                   _i64, _p, _p, _i64, ctypes.c_int, _i64, _p, ctypes.c_size_t, _p]),
+    "hc_mg_wait": (ctypes.c_int, [_p, _p, _p]),
     "hc_dist_boundary": (ctypes.c_int, [_p, _p, _i64, _i64, _p, _p]),
     "hc_dist_assign": (ctypes.c_int, [_p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p]),
     "hc_dist_resolve": (ctypes.c_int, [_p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p, _p, _p, _p]),

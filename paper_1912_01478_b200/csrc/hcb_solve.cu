@@ -55,6 +55,8 @@
 // Row offsets are read as int32 when num_edges < 2^31 (a copy made in the
 // preprocessing), halving the offset traffic; int64 otherwise.  Column loads
 // are streaming (evict-first) so the X gathers keep L2.
+#include <string.h>
+
 #include <algorithm>
 
 #include "hcb_partition.cuh"
@@ -105,7 +107,31 @@ struct Ctrl {
     long long rec_overflow;
     unsigned fmt_overflow;                       // a tentative color exceeded the state word
     unsigned pad1;
+    // multi-GPU: this rank's next-worklist size per parity, the global sums of
+    // the last round (|W'|, conflicts) and the abort flag of a timed-out barrier
+    unsigned long long wl_next[2];
+    unsigned long long g_wl, g_conf;
+    unsigned abort;
+    unsigned pad2;
     unsigned segcnt[2][NSEG_BINS][MAXSEG];       // [parity][bin][segment] loser counts
+};
+
+// Multi-GPU mailbox, one per rank, in the rank's peer-mapped shared region
+// (after its state-word replica).  Rank r's cross-GPU barrier number e posts
+// (e, payload) into slot [e & 1][r] of every rank's mailbox (st.release.sys)
+// and waits until all slots [e & 1][*] of its own mailbox reach e.  Two slot
+// sets suffice: a rank can post e+2 only after every rank posted e+1, i.e.
+// after every rank finished reading the payloads of e.
+constexpr int MG_MAX_WORLD = 8;
+struct MboxSlot {
+    unsigned long long epoch;
+    unsigned long long a, b;
+    unsigned long long pad;
+};
+struct Mbox {
+    MboxSlot slot[2][MG_MAX_WORLD];
+    unsigned long long last_epoch;  // barriers used by the previous solves (all ranks agree)
+    unsigned long long pad[3];
 };
 
 // per-hub merge slot for hubs split across several CTAs (latency regime)
@@ -137,6 +163,14 @@ struct Params {
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
     HubAcc *hub_acc;           // MAX_SPLIT_SLOTS merge slots (zeroed; reset by their last slice)
     unsigned *fmt_overflow;    // set when a tentative color does not fit the state word
+    long long lo, nown;        // owned node range [lo, lo + nown) (single GPU: 0, n)
+    // multi-GPU (Fmt::mg) only
+    const unsigned char *bnd;  // boundary flag, indexed by global node id (owned ids only)
+    void *const *peer_x;       // [world] every rank's state-word replica (device array)
+    Mbox *const *peer_mbox;    // [world] every rank's mailbox
+    Mbox *mbox;                // this rank's mailbox
+    int rank, world;
+    long long timeout_ns;      // cross-GPU barrier wait limit
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -174,6 +208,7 @@ struct Smem {
     int hub_first;
     unsigned unit;
     unsigned out_cnt;
+    unsigned mg_abort;
 };
 
 // dynamic list of parity p, bin b (selects instead of a runtime-indexed
@@ -226,21 +261,101 @@ __device__ __forceinline__ void mark(unsigned *bm, unsigned c) {
     atomicOr(&bm[(c - 1u) >> 5], 1u << ((c - 1u) & 31u));
 }
 
+// loser count of output segment c of bin `bin`; the multi-GPU solve also
+// keeps this rank's next-worklist total for the cross-GPU reduction
+template <bool MG>
+__device__ __forceinline__ void seg_put(const Params &P, int np, int bin, unsigned c, unsigned cnt) {
+    P.ctrl->segcnt[np][bin][c] = cnt;
+    if constexpr (MG) {
+        if (cnt) atomicAdd(&P.ctrl->wl_next[np], (unsigned long long)cnt);
+    }
+}
+
+// Cross-GPU barrier of the multi-GPU solve: the grid barrier whose last
+// arriving CTA exchanges (epoch, payload) with every rank's mailbox over
+// NVLink.  kind 0: plain;  kind 1: end of round t with parity p -- payload =
+// this rank's (|W_{t+1}|, conflicts of t), global sums left in C->g_wl /
+// C->g_conf for the next round's mode decision (driver.py:147-152) and record.
+// Every CTA fences its mirrored stores (fence.sc.sys) before arriving, so a
+// peer that passes the barrier sees them.  Returns false if some rank did not
+// arrive within P.timeout_ns (the whole grid then leaves the kernel).
+__device__ bool mg_sync(const Params &P, Smem &sm, unsigned long long epoch, int kind, int p) {
+    Ctrl *C = P.ctrl;
+    GridBarrier *b = &C->bar;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = ld_acquire_u32(&b->gen);
+        __threadfence_system();
+        const unsigned arrived = atomicAdd(&b->count, 1u);
+        if (arrived == P.nblocks - 1) {
+            atomicExch(&b->count, 0u);
+            __threadfence_system();
+            unsigned long long a = 0, c = 0;
+            if (kind == 1) {
+                a = __ldcg(&C->wl_next[p ^ 1]) + __ldcg(&C->hub_cnt[p ^ 1]);
+                c = __ldcg(&C->conflicts[p]);
+            }
+            const int par = (int)(epoch & 1ull);
+            for (int q = 0; q < P.world; ++q) {
+                MboxSlot *sl = &P.peer_mbox[q]->slot[par][P.rank];
+                st_relaxed_sys_u64(&sl->a, a);
+                st_relaxed_sys_u64(&sl->b, c);
+                st_release_sys_u64(&sl->epoch, epoch);
+            }
+            const unsigned long long t0 = globaltimer();
+            unsigned long long sa = 0, sc = 0;
+            unsigned ok = 1;
+            for (int q = 0; q < P.world && ok; ++q) {
+                MboxSlot *sl = &P.mbox->slot[par][q];
+                while (ld_acquire_sys_u64(&sl->epoch) < epoch) {
+                    if ((long long)(globaltimer() - t0) > P.timeout_ns) {
+                        ok = 0;
+                        break;
+                    }
+                    __nanosleep(32);
+                }
+                sa += ld_relaxed_sys_u64(&sl->a);
+                sc += ld_relaxed_sys_u64(&sl->b);
+            }
+            if (!ok) C->abort = 1u;
+            if (kind == 1) {
+                C->g_wl = sa;
+                C->g_conf = sc;
+            }
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
+        }
+        __threadfence();
+        sm.mg_abort = *(volatile unsigned *)&C->abort;
+    }
+    __syncthreads();
+    return sm.mg_abort == 0u;
+}
+
 // Storage formats, chosen per graph by hc_solve:
 //   state word  XT = uint32 (bit 31 = committed)  or uint16 (bit 15), the
 //               latter when max degree <= 16384 so every color fits 15 bits
 //   column id   CT = int32 absolute  or int16 delta (v - u), the latter when
 //               every |v - u| < 2^15 (grids / meshes with local numbering)
 // All solver logic works on the 32-bit encoding; the accessors convert.
-template <typename XT, typename CT>
+//   MG          multi-GPU (hc_mg_solve): this rank owns [lo, lo+nown); writes
+//               of owned boundary words are mirrored into every peer's replica
+template <typename XT, typename CT, bool MG = false>
 struct Fmt {
     using xt = XT;
     using ct = CT;
+    static constexpr bool mg = MG;
 };
 using F32 = Fmt<unsigned, int>;
 using F16 = Fmt<unsigned short, int>;
 using F16D = Fmt<unsigned short, short>;
 using F32D = Fmt<unsigned, short>;
+using MF32 = Fmt<unsigned, int, true>;
+using MF16 = Fmt<unsigned short, int, true>;
+using MF16D = Fmt<unsigned short, short, true>;
+using MF32D = Fmt<unsigned, short, true>;
 
 // committed flag / color mask of the format's state word; words are kept
 // zero-extended in registers, so no conversion on load or store
@@ -253,9 +368,27 @@ template <class F>
 __device__ __forceinline__ unsigned xget(const Params &P, long long v) {
     return reinterpret_cast<const typename F::xt *>(P.X)[v];
 }
+// store to the local word only (initialisation)
+template <class F>
+__device__ __forceinline__ void xraw(const Params &P, long long v, unsigned w) {
+    reinterpret_cast<typename F::xt *>(P.X)[v] = (typename F::xt)w;
+}
+// multi-GPU: the word of an owned boundary node is also stored into every
+// peer's replica (NVLink stores; made visible by the fence.sys of the next
+// cross-GPU barrier).  Interior words are read by no other rank.
+template <class F>
+__device__ __noinline__ void mirror(const Params &P, long long v, unsigned w) {
+    for (int q = 0; q < P.world; ++q)
+        if (q != P.rank)
+            reinterpret_cast<typename F::xt *>(__ldg(reinterpret_cast<const unsigned long long *>(P.peer_x) + q))[v] =
+                (typename F::xt)w;
+}
 template <class F>
 __device__ __forceinline__ void xput(const Params &P, long long v, unsigned w) {
     reinterpret_cast<typename F::xt *>(P.X)[v] = (typename F::xt)w;
+    if constexpr (F::mg) {
+        if (__ldg(P.bnd + v)) mirror<F>(P, v, w);
+    }
 }
 // tentative color write: a 16-bit word cannot hold T > 32767 (possible only
 // for degree > 32766); flag it, the host reruns the solve with 32-bit words
@@ -497,7 +630,7 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
     for (int j = 0; j < NPT; ++j) {
         const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
-        u[j] = v < hi ? (ident ? (int)v : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
+        u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
         lost[j] = false;
         xu[j] = 0u;
     }
@@ -604,7 +737,7 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
         group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out,
                                           &sm.out_cnt, sm.win_bm[warp], my_conf, my_edges);
     __syncthreads();
-    if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][bin][c] = sm.out_cnt;
+    if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, c, sm.out_cnt);
 }
 
 // ------------------------------------------------------------------ split hubs
@@ -806,7 +939,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
                 }
             }
         }
-        if (!is_hub && PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][3][c] = pushed;
+        if (!is_hub && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 3, c, pushed);
     } else if (unit < ub[2]) {
         group_chunk<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
     } else if (unit < ub[3]) {
@@ -856,7 +989,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
                 buf ^= 1u;
             }
         }
-        if (PHASE == 1 && threadIdx.x == 0) P.ctrl->segcnt[np][0][c] = written;
+        if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 0, c, written);
     }
 }
 
@@ -889,7 +1022,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
     const long long gthreads = (long long)P.nblocks * BLOCK;
     RoundCfg &rc = sm.rc;
 
-    for (long long u = gtid; u < P.n; u += gthreads) xput<F>(P, u, 0u);
+    for (long long u = gtid; u < P.n; u += gthreads) xraw<F>(P, u, 0u);
     if (threadIdx.x == 0) {
         unsigned long long off = 0;
         for (int b = 0; b < NBIN; ++b) {
@@ -897,10 +1030,19 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
             rc.stat_lists[b] = P.stat + off;
             off += rc.nst[b];
         }
-        rc.ident_small = rc.nst[0] == (unsigned long long)P.n;  // all nodes in bin 0: sweep ids
+        rc.ident_small = rc.nst[0] == (unsigned long long)P.nown;  // all nodes in bin 0: sweep ids
         for (int b = 0; b < NSEG_BINS; ++b) rc.prev_nseg[b] = rc.prev_cap[b] = 0;
     }
-    grid_sync(&C->bar, P.nblocks);
+    // multi-GPU: barrier epochs continue from the previous solve (every rank
+    // runs the same number of barriers); the first barrier also guarantees
+    // every replica is zeroed before any peer mirrors into it
+    unsigned long long ep = 0;
+    if constexpr (F::mg) {
+        ep = *(volatile unsigned long long *)&P.mbox->last_epoch;
+        if (!mg_sync(P, sm, ++ep, 0, 0)) return;
+    } else {
+        grid_sync(&C->bar, P.nblocks);
+    }
 
     unsigned long long t_start = 0;  // block 0 / thread 0 record keeping
     long long wl_in_prev = 0;
@@ -959,9 +1101,11 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
                                         rc.prev_cap[b], true};
             const unsigned long long hub_total = t == 1 ? rc.nst[BIN_HUB] : ld_relaxed_u64(&C->hub_cnt[p]);
             rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : dyn_list(P, p, BIN_HUB), hub_total, 0, 0, false};
-            unsigned long long s = 0;
+            unsigned long long s = 0;  // this rank's |W_t| (the whole |W_t| on one GPU)
             for (int b = 0; b < NBIN; ++b) s += rc.L[b].total;
-            const bool topo = P.mode == HC_MODE_TOPO || (P.mode == HC_MODE_HYBRID && (long long)s > P.thr);
+            // global |W_t|: multi-GPU sums over ranks at the end-of-round barrier
+            const unsigned long long sg = !F::mg ? s : t == 1 ? (unsigned long long)P.n : __ldcg(&C->g_wl);
+            const bool topo = P.mode == HC_MODE_TOPO || (P.mode == HC_MODE_HYBRID && (long long)sg > P.thr);
             // bin-3 nodes at CTA granularity when few are active (latency regime)
             const bool bin3_cta = rc.L[3].total <= 2ull * P.nblocks;
             if (topo)  // topology-driven: sweep the static lists, activity test
@@ -986,7 +1130,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
             rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
             rc.ubase[5] = rc.ubase[4] + (live ? rc.nch[0] : 0u);
-            sm.red = s;  // broadcast |W_t|
+            sm.red = sg;  // broadcast |W_t|
             if (blockIdx.x == 0) {
                 const unsigned long long now = globaltimer();
                 if (t > 1) {  // finish the record of round t-1 (driver.py:159-168)
@@ -996,17 +1140,18 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
                         r.round = t - 1;
                         r.topo = topo_prev;
                         r.wl_in = wl_in_prev;
-                        r.wl_out = (long long)s;
-                        r.conflicts = (long long)C->conflicts[q];
+                        r.wl_out = (long long)sg;
+                        r.conflicts = F::mg ? (long long)__ldcg(&C->g_conf) : (long long)C->conflicts[q];
                         r.ns = (long long)(now - t_start);
                         P.rec[t - 2] = r;
                     }
                     C->conflicts[q] = 0;
                     C->hub_cnt[q] = 0;
+                    C->wl_next[q] = 0;
                     C->unit_ctr[0][q] = C->unit_ctr[1][q] = 0;
                 }
                 t_start = now;
-                wl_in_prev = (long long)s;
+                wl_in_prev = (long long)sg;
                 topo_prev = topo;
             }
         }
@@ -1044,7 +1189,11 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         }
 
         run_phase<OffT, F, STATS, 0>(P, ro, sm, p, my_conf, my_edges);
-        grid_sync(&C->bar, P.nblocks);
+        if constexpr (F::mg) {
+            if (!mg_sync(P, sm, ++ep, 0, p)) return;  // peers' tentative colors are in
+        } else {
+            grid_sync(&C->bar, P.nblocks);
+        }
         run_phase<OffT, F, STATS, 1>(P, ro, sm, p, my_conf, my_edges);
 
         // conflicts of this round: block reduce then one atomic per CTA
@@ -1070,13 +1219,19 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
                 rc.prev_nseg[b] = rc.nch[b];
                 rc.prev_cap[b] = rc.csz[b];
             }
-        grid_sync(&C->bar, P.nblocks);
+        if constexpr (F::mg) {
+            if (!mg_sync(P, sm, ++ep, 1, p)) return;  // winners in; global (|W'|, conflicts)
+        } else {
+            grid_sync(&C->bar, P.nblocks);
+        }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->rounds = t - 1;
         if (t - 1 > P.max_rec) C->rec_overflow = 1;
+        if constexpr (F::mg) P.mbox->last_epoch = ep;
     }
-    for (long long u = gtid; u < P.n; u += gthreads) P.colors_out[u] = (long long)(xget<F>(P, u) & CM<F>);
+    for (long long i = gtid; i < P.nown; i += gthreads)
+        P.colors_out[i] = (long long)(xget<F>(P, P.lo + i) & CM<F>);
 }
 
 // Static lists: nodes bucket-sorted by a degree key.  Keys 0-2 are bins 0-2;
@@ -1099,7 +1254,8 @@ struct DegreeKey {
     }
 };
 struct EmitI32 {
-    __device__ int operator()(long long i) const { return (int)i; }
+    long long lo;  // first owned node (multi-GPU), 0 on one GPU
+    __device__ int operator()(long long i) const { return (int)(lo + i); }
 };
 
 __global__ void copy_totals_kernel(const unsigned long long *tot, Ctrl *c) {
@@ -1117,11 +1273,11 @@ __global__ void narrow_offsets_kernel(const long long *ro, int *ro32, long long 
 
 // int16 delta columns ci16[k] = ci[k] - u; sets *bad when some |v-u| >= 2^15
 // (then the absolute int32 columns are used).  Warp per row, early exit.
-__global__ void delta_columns_kernel(const long long *ro, const int *ci, long long n, short *ci16,
-                                     unsigned *bad) {
+__global__ void delta_columns_kernel(const long long *ro, const int *ci, long long lo, long long hi,
+                                     short *ci16, unsigned *bad) {
     const unsigned lane = lane_id();
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
+    for (long long u = lo + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < hi; u += nwarps) {
         if (*(volatile unsigned *)bad) return;
         bool over = false;
         for (long long k = ro[u] + lane; k < ro[u + 1]; k += 32) {
@@ -1136,32 +1292,49 @@ __global__ void delta_columns_kernel(const long long *ro, const int *ci, long lo
     }
 }
 
+// max degree over all nodes (the multi-GPU state-word format must agree on
+// every rank, so it is decided from the whole graph)
+__global__ void max_degree_kernel(const long long *ro, long long n, unsigned long long *out) {
+    unsigned long long d = 0;
+    for (long long u = (long long)blockIdx.x * blockDim.x + threadIdx.x; u < n; u += (long long)gridDim.x * blockDim.x)
+        d = max(d, (unsigned long long)(ro[u + 1] - ro[u]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d = max(d, __shfl_xor_sync(FULL, d, o));
+    if (lane_id() == 0 && d) atomicMax(out, d);
+}
+
 // worst-case segmented capacity of a bin with `cnt` static nodes
 inline size_t seg_capacity(long long cnt) {
     return (size_t)cnt + (size_t)cnt / MAXSEG + 2 * BLOCK * NPT;
 }
 
 struct Layout {
-    size_t x, stat, dyn[2][NBIN], ro32, ci16, hub_acc, ctrl, part, total;
+    size_t ctrl, x, stat, dyn[2][NBIN], ro32, ci16, hub_acc, part, bnd, ptrs, maxdeg, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
-// the device; size each for the whole node count (upper bound of every bin).
-static Layout layout(long long n, long long m) {
+// the device; size each for the whole owned node count (upper bound of every
+// bin).  The control block comes first (hc_mg_wait finds it there).  The
+// multi-GPU layout has no state words (they live in the peer-mapped shared
+// region) but boundary flags and the peer pointer tables.
+static Layout layout(long long n, long long m, long long nown, bool mg) {
     Layout L;
     size_t o = 0;
-    L.x = o; o = align_up(o + 4 * (size_t)n, 256);
-    L.stat = o; o = align_up(o + 4 * (size_t)n, 256);
+    L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
+    L.x = o; o = align_up(o + (mg ? 0 : 4 * (size_t)n), 256);
+    L.stat = o; o = align_up(o + 4 * (size_t)nown, 256);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) {
             L.dyn[p][b] = o;
-            o = align_up(o + 4 * (b == BIN_HUB ? (size_t)n : seg_capacity(n)), 256);
+            o = align_up(o + 4 * (b == BIN_HUB ? (size_t)nown : seg_capacity(nown)), 256);
         }
     L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
     L.ci16 = o; o = align_up(o + (m < 0x7fffffffLL ? 2 * (size_t)m : 0) + 256, 256);
     L.hub_acc = o; o = align_up(o + sizeof(HubAcc) * MAX_SPLIT_SLOTS, 256);
-    L.ctrl = o; o = align_up(o + sizeof(Ctrl), 256);
-    L.part = o; o = align_up(o + part_scratch_bytes(NKEY, n), 256);
+    L.part = o; o = align_up(o + part_scratch_bytes(NKEY, nown), 256);
+    L.bnd = o; o = align_up(o + (mg ? (size_t)nown : 0), 256);
+    L.ptrs = o; o = align_up(o + (mg ? 2 * sizeof(void *) * MG_MAX_WORLD : 0), 256);
+    L.maxdeg = o; o = align_up(o + 8, 256);
     L.total = o;
     return L;
 }
@@ -1178,6 +1351,15 @@ static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats) {
     if (x16) return stats ? kernel_ptr<int, F16, true>() : kernel_ptr<int, F16, false>();
     if (c16) return stats ? kernel_ptr<int, F32D, true>() : kernel_ptr<int, F32D, false>();
     return stats ? kernel_ptr<int, F32, true>() : kernel_ptr<int, F32, false>();
+}
+
+// multi-GPU instantiations (no per-round edge statistics)
+static const void *select_kernel_mg(bool narrow, bool x16, bool c16) {
+    if (!narrow) return x16 ? kernel_ptr<long long, MF16, false>() : kernel_ptr<long long, MF32, false>();
+    if (x16 && c16) return kernel_ptr<int, MF16D, false>();
+    if (x16) return kernel_ptr<int, MF16, false>();
+    if (c16) return kernel_ptr<int, MF32D, false>();
+    return kernel_ptr<int, MF32, false>();
 }
 
 static int occupancy_of(const void *fn) {
@@ -1197,6 +1379,85 @@ static int occupancy() {
 // format overrides (tests / experiments): force int64 offsets, forbid the
 // 16-bit state word, forbid 16-bit delta columns
 static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0;
+
+// Per-solve preprocessing shared by hc_solve and hc_mg_solve, for the owned
+// range [lo, lo + nown): fresh control block, static degree-bucketed lists,
+// int32 offsets, int16 delta columns; reads back the bucket totals, the
+// delta-column verdict and (multi-GPU) the whole graph's max degree.
+struct Prep {
+    unsigned long long tot[NKEY];
+    unsigned long long *d_totals;
+    bool narrow, c16_ok;
+    unsigned long long max_degree;
+};
+
+static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_offsets, long long n,
+                   long long m, bool want_maxdeg, Prep &out, cudaStream_t st) {
+    const bool narrow = m < 0x7fffffffLL && !g_force_wide;
+    out.narrow = narrow;
+    P.ctrl = reinterpret_cast<Ctrl *>(ws + L.ctrl);
+    HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
+    P.hub_acc = reinterpret_cast<HubAcc *>(ws + L.hub_acc);
+    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
+    P.stat = reinterpret_cast<int *>(ws + L.stat);
+    for (int p = 0; p < 2; ++p)
+        for (int b = 0; b < NBIN; ++b) P.dyn[p][b] = reinterpret_cast<int *>(ws + L.dyn[p][b]);
+    P.fmt_overflow = &P.ctrl->fmt_overflow;
+    const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
+    P.ro = narrow ? (const void *)(ws + L.ro32) : (const void *)d_row_offsets;
+    // static degree-bucketed lists of the owned nodes (bins contiguous, see DegreeKey)
+    int rc = bucket_sort<NKEY>(P.nown, DegreeKey{ro64 + P.lo}, EmitI32{P.lo}, P.stat, ws + L.part,
+                               &out.d_totals, st);
+    if (rc != HC_OK) return rc;
+    const int sms = std::max(1, num_sms());
+    copy_totals_kernel<<<1, 32, 0, st>>>(out.d_totals, P.ctrl);
+    HC_CHECK_LAUNCH();
+    if (narrow) {
+        narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro64, reinterpret_cast<int *>(ws + L.ro32), n + 1);
+        HC_CHECK_LAUNCH();
+    }
+    // int16 delta columns of the owned rows when every |v - u| < 2^15
+    unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? 2 * (size_t)m : 0));
+    HC_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
+    P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
+    if (narrow && m > 0 && P.nown > 0) {
+        delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro64, P.ci, P.lo, P.lo + P.nown,
+                                                      reinterpret_cast<short *>(ws + L.ci16), bad);
+        HC_CHECK_LAUNCH();
+    }
+    unsigned long long *d_maxdeg = reinterpret_cast<unsigned long long *>(ws + L.maxdeg);
+    out.max_degree = 0;
+    if (want_maxdeg) {
+        HC_CUDA_TRY(cudaMemsetAsync(d_maxdeg, 0, 8, st));
+        max_degree_kernel<<<sms * 4, 256, 0, st>>>(ro64, n, d_maxdeg);
+        HC_CHECK_LAUNCH();
+    }
+    unsigned h_bad = 1;
+    HC_CUDA_TRY(cudaMemcpyAsync(out.tot, out.d_totals, sizeof out.tot, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, st));
+    if (want_maxdeg)
+        HC_CUDA_TRY(cudaMemcpyAsync(&out.max_degree, d_maxdeg, 8, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    out.c16_ok = (HC_FMT16 != 0) && !g_no_c16 && narrow && m > 0 && h_bad == 0;
+    return HC_OK;
+}
+
+// the multi-GPU shared region of a rank: state-word replica, then mailbox
+inline size_t mg_x_bytes(long long n) { return align_up(4 * (size_t)std::max(n, 1LL), 256); }
+
+// driver API entry point (no -lcuda link: the library must load without a GPU)
+typedef int (*MemGetAddressRangeFn)(unsigned long long *, size_t *, unsigned long long);
+static MemGetAddressRangeFn mem_get_address_range() {
+    static MemGetAddressRangeFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (MemGetAddressRangeFn)p;
+    }
+    return fn;
+}
 
 }  // namespace solve
 }  // namespace hcb
@@ -1220,8 +1481,8 @@ int hc_device_info(int *h_num_sms, int *h_ctas_per_sm) {
 }
 
 size_t hc_solve_workspace_bytes(int64_t num_nodes, int64_t num_edges) {
-    (void)num_edges;
-    return layout(num_nodes < 0 ? 0 : num_nodes, num_edges < 0 ? 0 : num_edges).total;
+    const long long n = num_nodes < 0 ? 0 : num_nodes;
+    return layout(n, num_edges < 0 ? 0 : num_edges, n, false).total;
 }
 
 int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
@@ -1246,20 +1507,16 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     if (num_nodes == 0) return HC_OK;  // empty graph: 0 rounds (test_driver.py:88-93)
     HC_REQUIRE(d_row_offsets && d_colors && (num_edges == 0 || d_col_indices), HC_ERR_INVALID,
                "hc_solve: null pointer");
-    const Layout L = layout(num_nodes, num_edges);
+    const Layout L = layout(num_nodes, num_edges, num_nodes, false);
     HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
                "hc_solve: workspace %zu bytes < required %zu", ws_bytes, L.total);
     char *ws = reinterpret_cast<char *>(d_ws);
-    const bool narrow = num_edges < 0x7fffffffLL && !g_force_wide;
-    Params P;
-    P.ro = narrow ? (const void *)(ws + L.ro32) : (const void *)d_row_offsets;
+    Params P{};
     P.ci = d_col_indices;
     P.n = num_nodes;
+    P.lo = 0;
+    P.nown = num_nodes;
     P.X = reinterpret_cast<unsigned *>(ws + L.x);
-    P.stat = reinterpret_cast<int *>(ws + L.stat);
-    for (int p = 0; p < 2; ++p)
-        for (int b = 0; b < NBIN; ++b) P.dyn[p][b] = reinterpret_cast<int *>(ws + L.dyn[p][b]);
-    P.ctrl = reinterpret_cast<Ctrl *>(ws + L.ctrl);
     P.rec = d_rec;
     P.max_rec = d_rec ? max_rec : 0;
     P.colors_out = reinterpret_cast<long long *>(d_colors);
@@ -1268,62 +1525,32 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     P.stats = reinterpret_cast<long long *>(d_stats);
     if (d_stats && P.max_rec)
         HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
-
-    HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
-    P.hub_acc = reinterpret_cast<HubAcc *>(ws + L.hub_acc);
-    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
-    const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
-    // static degree-bucketed lists (bins contiguous, see DegreeKey)
-    unsigned long long *totals = nullptr;
-    int rc = bucket_sort<NKEY>(num_nodes, DegreeKey{ro64}, EmitI32{}, P.stat, ws + L.part, &totals, st);
+    Prep pr;
+    int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, false, pr, st);
     if (rc != HC_OK) return rc;
-    const int sms = std::max(1, num_sms());
-    copy_totals_kernel<<<1, 32, 0, st>>>(totals, P.ctrl);
-    HC_CHECK_LAUNCH();
-    if (narrow) {
-        narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro64, reinterpret_cast<int *>(ws + L.ro32),
-                                                       num_nodes + 1);
-        HC_CHECK_LAUNCH();
-    }
 
-    // storage formats (see Fmt): 16-bit state words when max degree <= 16384
-    // (no node in the hub buckets >= 16385), 16-bit delta columns when every
-    // |v - u| < 2^15
-    unsigned long long h_tot[NKEY];
-    unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? 2 * (size_t)num_edges : 0));
-    HC_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
-    P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
-    if (narrow && num_edges > 0) {
-        delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro64, d_col_indices, num_nodes,
-                                                      reinterpret_cast<short *>(ws + L.ci16), bad);
-        HC_CHECK_LAUNCH();
-    }
-    unsigned h_bad = 1;
-    HC_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, st));
-    HC_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof h_bad, cudaMemcpyDeviceToHost, st));
-    HC_CUDA_TRY(cudaStreamSynchronize(st));
-    // 16-bit words are exact when max degree <= 16384 (mex <= 16385); above
-    // that they are used speculatively and the solve is redone with 32-bit
-    // words if any tentative color overflows (never for the BASELINE graphs)
-    const bool x16_exact = h_tot[9] + h_tot[10] + h_tot[11] + h_tot[12] == 0;
+    // 16-bit state words are exact when max degree <= 16384 (mex <= 16385;
+    // no node in the hub buckets >= 16385); above that they are used
+    // speculatively and the solve is redone with 32-bit words if any tentative
+    // color overflows (never for the BASELINE graphs)
+    const bool x16_exact = pr.tot[9] + pr.tot[10] + pr.tot[11] + pr.tot[12] == 0;
     bool x16 = (HC_FMT16 != 0) && !g_no_x16;
-    const bool c16 = (HC_FMT16 != 0) && !g_no_c16 && narrow && num_edges > 0 && h_bad == 0;
+    const bool c16 = pr.c16_ok;
     const int per_sm = occupancy();
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
-    P.nblocks = (unsigned)(per_sm * sms);
-    P.fmt_overflow = &P.ctrl->fmt_overflow;
+    P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
     long long info[3];
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) {  // fresh control block (keeps nstat via copy_totals)
             HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
-            copy_totals_kernel<<<1, 32, 0, st>>>(totals, P.ctrl);
+            copy_totals_kernel<<<1, 32, 0, st>>>(pr.d_totals, P.ctrl);
             HC_CHECK_LAUNCH();
             HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
             if (d_stats && P.max_rec)
                 HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
         }
         void *args[] = {&P};
-        const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr);
+        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr);
         HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
         HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
         HC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1334,6 +1561,138 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     if (h_rounds) *h_rounds = info[0];
     HC_REQUIRE(!info[1], HC_ERR_RECORDS, "hc_solve: %lld rounds exceed the %lld-record buffer",
                info[0], (long long)max_rec);
+    return HC_OK;
+}
+
+/* ---------------------------------------------------------------- multi-GPU */
+
+size_t hc_mg_shared_bytes(int64_t num_nodes) {
+    return mg_x_bytes(num_nodes < 0 ? 0 : num_nodes) + align_up(sizeof(Mbox), 256);
+}
+
+size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t num_edges, int64_t lo, int64_t hi) {
+    const long long n = num_nodes < 0 ? 0 : num_nodes;
+    const long long nown = hi > lo ? hi - lo : 0;
+    return layout(n, num_edges < 0 ? 0 : num_edges, nown, true).total;
+}
+
+int hc_mg_ipc_export(const void *d_ptr, void *h_handle, int64_t *h_offset) {
+    HC_REQUIRE(d_ptr && h_handle && h_offset, HC_ERR_INVALID, "hc_mg_ipc_export: null pointer");
+    MemGetAddressRangeFn range = mem_get_address_range();
+    HC_REQUIRE(range, HC_ERR_CUDA, "hc_mg_ipc_export: cuMemGetAddressRange unavailable");
+    unsigned long long base = 0;
+    size_t size = 0;
+    HC_REQUIRE(range(&base, &size, (unsigned long long)(uintptr_t)d_ptr) == 0, HC_ERR_CUDA,
+               "hc_mg_ipc_export: cuMemGetAddressRange failed");
+    cudaIpcMemHandle_t h;
+    HC_CUDA_TRY(cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+    static_assert(sizeof(cudaIpcMemHandle_t) == HC_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(h_handle, &h, sizeof h);
+    *h_offset = (int64_t)((uintptr_t)d_ptr - (uintptr_t)base);
+    return HC_OK;
+}
+
+int hc_mg_ipc_import(const void *h_handle, int64_t offset, void **h_dptr) {
+    HC_REQUIRE(h_handle && h_dptr && offset >= 0, HC_ERR_INVALID, "hc_mg_ipc_import: bad arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, h_handle, sizeof h);
+    void *base = nullptr;
+    HC_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *h_dptr = (char *)base + offset;
+    return HC_OK;
+}
+
+int hc_mg_ipc_close(void *d_ptr, int64_t offset) {
+    HC_REQUIRE(d_ptr && offset >= 0, HC_ERR_INVALID, "hc_mg_ipc_close: bad arguments");
+    HC_CUDA_TRY(cudaIpcCloseMemHandle((char *)d_ptr - offset));
+    return HC_OK;
+}
+
+int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
+    HC_REQUIRE(num_nodes >= 1 && num_nodes < 0x7fffffffLL, HC_ERR_INVALID,
+               "hc_mg_solve: num_nodes %lld out of range", (long long)num_nodes);
+    HC_REQUIRE(num_edges >= 0, HC_ERR_INVALID, "hc_mg_solve: num_edges < 0");
+    HC_REQUIRE(world >= 1 && world <= MG_MAX_WORLD && rank >= 0 && rank < world, HC_ERR_INVALID,
+               "hc_mg_solve: rank %d / world %d invalid (world <= %d)", rank, world, MG_MAX_WORLD);
+    HC_REQUIRE(lo >= 0 && hi >= lo && hi <= num_nodes, HC_ERR_INVALID, "hc_mg_solve: bad owned range");
+    HC_REQUIRE(mode >= HC_MODE_DATA && mode <= HC_MODE_HYBRID, HC_ERR_INVALID,
+               "hc_mg_solve: mode %d invalid", mode);
+    HC_REQUIRE(max_rec >= 0 && ctas >= 0, HC_ERR_INVALID, "hc_mg_solve: bad max_rec / ctas");
+    HC_REQUIRE(d_row_offsets && (num_edges == 0 || d_col_indices) && h_shared &&
+                   (hi == lo || d_colors), HC_ERR_INVALID, "hc_mg_solve: null pointer");
+    for (int q = 0; q < world; ++q) HC_REQUIRE(h_shared[q], HC_ERR_INVALID, "hc_mg_solve: null shared[%d]", q);
+    cudaStream_t st = as_stream(stream);
+    const Layout L = layout(num_nodes, num_edges, hi - lo, true);
+    HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
+               "hc_mg_solve: workspace %zu bytes < required %zu", ws_bytes, L.total);
+    char *ws = reinterpret_cast<char *>(d_ws);
+    Params P{};
+    P.ci = d_col_indices;
+    P.n = num_nodes;
+    P.lo = lo;
+    P.nown = hi - lo;
+    P.rec = d_rec;
+    P.max_rec = d_rec ? max_rec : 0;
+    P.colors_out = reinterpret_cast<long long *>(d_colors);
+    P.mode = mode;
+    P.thr = thr_count;
+    P.rank = rank;
+    P.world = world;
+    P.timeout_ns = (timeout_ms > 0 ? timeout_ms : 60000) * 1000000LL;
+    Prep pr;
+    int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, true, pr, st);
+    if (rc != HC_OK) return rc;
+    // boundary flags of the owned nodes (a neighbour outside [lo, hi))
+    unsigned char *bnd = reinterpret_cast<unsigned char *>(ws + L.bnd);
+    rc = hc_dist_boundary(d_row_offsets, d_col_indices, lo, hi, bnd, stream);
+    if (rc != HC_OK) return rc;
+    P.bnd = bnd - lo;
+    // peer tables: every rank's replica and mailbox (pointers valid in this process)
+    void *tab[2 * MG_MAX_WORLD] = {};
+    for (int q = 0; q < world; ++q) {
+        tab[q] = h_shared[q];
+        tab[MG_MAX_WORLD + q] = (char *)h_shared[q] + mg_x_bytes(num_nodes);
+    }
+    void **d_tab = reinterpret_cast<void **>(ws + L.ptrs);
+    HC_CUDA_TRY(cudaMemcpyAsync(d_tab, tab, sizeof tab, cudaMemcpyHostToDevice, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    P.peer_x = d_tab;
+    P.peer_mbox = reinterpret_cast<Mbox *const *>(d_tab + MG_MAX_WORLD);
+    P.X = h_shared[rank];
+    P.mbox = reinterpret_cast<Mbox *>(tab[MG_MAX_WORLD + rank]);
+    // every rank must pick the same state-word width: decided on the whole graph
+    const bool x16 = (HC_FMT16 != 0) && !g_no_x16 && pr.max_degree <= 16384ull;
+    const void *fn = select_kernel_mg(pr.narrow, x16, pr.c16_ok);
+    const int per_sm = occupancy_of(fn);
+    HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_mg_solve: occupancy query failed");
+    const unsigned full = (unsigned)(per_sm * std::max(1, num_sms()));
+    P.nblocks = ctas > 0 ? std::min((unsigned)ctas, full) : full;
+    void *args[] = {&P};
+    if (ctas > 0)  // caller-sized grid (several ranks sharing one GPU): regular launch
+        HC_CUDA_TRY(cudaLaunchKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
+    else
+        HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
+    return HC_OK;  // asynchronous: hc_mg_wait collects the outcome
+}
+
+int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream) {
+    HC_REQUIRE(d_ws, HC_ERR_INVALID, "hc_mg_wait: null workspace");
+    cudaStream_t st = as_stream(stream);
+    const Ctrl *C = reinterpret_cast<const Ctrl *>(d_ws);  // the control block leads the layout
+    struct {
+        long long rounds, rec_overflow;
+    } info;
+    unsigned abort = 0;
+    HC_CUDA_TRY(cudaMemcpyAsync(&info, &C->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaMemcpyAsync(&abort, &C->abort, sizeof abort, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    HC_REQUIRE(!abort, HC_ERR_TIMEOUT, "hc_mg_solve: a peer did not reach a cross-GPU barrier in time");
+    if (h_rounds) *h_rounds = info.rounds;
+    HC_REQUIRE(!info.rec_overflow, HC_ERR_RECORDS, "hc_mg_solve: %lld rounds exceed the record buffer",
+               info.rounds);
     return HC_OK;
 }
 

@@ -1,0 +1,293 @@
+"""Device-resident multi-GPU hybrid IPGC over NVLink peer memory
+(include/hcb.h hc_mg_*).
+
+The reference has one process and one round loop (driver.py:122-176).  Here
+the node range is cut into P contiguous, edge-balanced ranges; rank p owns
+[lo_p, hi_p) and runs ONE persistent kernel for the whole solve -- the
+single-GPU solver (hcb_solve.cu) instantiated with the multi-GPU format:
+
+  * every rank keeps a replica of the state words X[n] in its *shared region*
+    (plus a mailbox); all ranks' regions are mapped into every rank
+    (cudaIpc handles exchanged over torch.distributed, NVLink P2P mappings);
+  * the word of an owned *boundary* node (a neighbour outside the range) is
+    stored straight into every peer's replica by the thread that computes it
+    -- the exchange is fused into assign / resolve, no pack / collective /
+    unpack step;
+  * the two grid barriers of a round are cross-GPU barriers (fence.sc.sys,
+    then mailbox flags with st.release.sys / ld.acquire.sys); the end-of-round
+    one also all-reduces (|W'|, conflicts), so every rank takes the identical
+    hybrid decision (driver.py:147-152) and terminates in the same round.
+
+No host round trip per round.  Round semantics read only the previous
+snapshot (assign) and same-round tentatives (resolve) with id tie-breaks, so
+colors, round count and every per-round record equal the single-GPU solve
+(and the reference) for every partition.
+
+`virtual_color_graph` runs P ranks in one process on one GPU (one stream and
+a 1/P share of the SMs per rank, pointers instead of IPC mappings): the same
+kernel, barrier and mirroring code, testable on a single B200.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .driver import HybridConfig, RoundRecord, RunReport, threshold_count
+from .graph import DeviceCsr
+
+MAX_WORLD = 8
+IPC_HANDLE_BYTES = 64
+HC_ERR_TIMEOUT = -8
+
+
+def partition_bounds_device(row_offsets: torch.Tensor, world: int) -> list[tuple[int, int]]:
+    """Edge-balanced contiguous ranges, identical to distributed.partition_bounds
+    (cut p = first node whose row starts at or after m*p/P), computed on the
+    device with one searchsorted."""
+    n = int(row_offsets.numel()) - 1
+    m = int(row_offsets[-1].item()) if n >= 0 else 0
+    if m > 0 and world > 1:
+        targets = torch.tensor([(m * p) // world for p in range(1, world)], dtype=torch.int64,
+                               device=row_offsets.device)
+        raw = torch.searchsorted(row_offsets, targets, side="left").tolist()
+    else:
+        raw = [(n * p) // world for p in range(1, world)]
+    cuts = [0]
+    for c in raw:
+        cuts.append(min(max(int(c), cuts[-1]), n))
+    cuts.append(n)
+    return [(cuts[p], cuts[p + 1]) for p in range(world)]
+
+
+class RankSolver:
+    """One rank's reusable solve state for the owned range [lo, hi):
+    workspace, owned colors and the (global) per-round records."""
+
+    def __init__(self, graph: DeviceCsr, lo: int, hi: int, rank: int, world: int,
+                 shared_ptrs: list[int], *, max_rec: int | None = None, ctas: int = 0,
+                 timeout_ms: int = 60000):
+        if not 1 <= world <= MAX_WORLD:
+            raise ValueError(f"world size {world} not in [1, {MAX_WORLD}]")
+        self.L = _lib.load()
+        self.g = graph
+        self.lo, self.hi, self.rank, self.world = int(lo), int(hi), int(rank), int(world)
+        dev = graph.device
+        n = graph.num_nodes
+        self.ws = _lib.workspace(self.L.hc_mg_workspace_bytes(n, graph.num_edges, self.lo, self.hi), dev)
+        self.colors = torch.empty(max(self.hi - self.lo, 1), dtype=torch.int64, device=dev)
+        self.max_rec = int(max_rec if max_rec is not None else max(1, min(n, 1 << 20)))
+        self.rec = torch.empty((self.max_rec, _lib.REC_FIELDS), dtype=torch.int64, device=dev)
+        self.shared = (ctypes.c_void_p * world)(*[ctypes.c_void_p(p) for p in shared_ptrs])
+        self.ctas = int(ctas)
+        self.timeout_ms = int(timeout_ms)
+
+    def launch(self, mode: str, thr_count: int, stream: torch.cuda.Stream | None = None) -> None:
+        g = self.g
+        _lib.check(self.L.hc_mg_solve(
+            g.row_offsets.data_ptr(), _lib.ptr(g.col_indices), g.num_nodes, g.num_edges,
+            self.lo, self.hi, self.rank, self.world, ctypes.cast(self.shared, ctypes.c_void_p),
+            _lib.MODE_CODES[mode], int(thr_count),
+            self.colors.data_ptr(), self.rec.data_ptr(), self.max_rec, self.ctas, self.timeout_ms,
+            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(stream)))
+
+    def wait(self, stream: torch.cuda.Stream | None = None) -> int:
+        rounds = ctypes.c_int64(0)
+        _lib.check(self.L.hc_mg_wait(self.ws.data_ptr(), ctypes.byref(rounds), _lib.stream_handle(stream)))
+        return int(rounds.value)
+
+    def records(self, rounds: int) -> np.ndarray:
+        return self.rec[:rounds].cpu().numpy()
+
+
+def _report(graph_name, dg, config, recs, rounds, seconds) -> RunReport:
+    report = RunReport(graph_name, dg.num_nodes, dg.num_undirected_edges, config)
+    for r in recs:
+        report.per_round.append(RoundRecord(
+            round=int(r[0]), mode_used="topo" if r[1] else "data", worklist_size_in=int(r[2]),
+            worklist_size_out=int(r[3]), conflicts=int(r[4]), wall_seconds=float(r[5]) * 1e-9))
+    report.total_rounds = rounds
+    report.total_seconds = seconds
+    return report
+
+
+@dataclass
+class MgResult:
+    colors: np.ndarray          # int64[n], the whole coloring
+    report: RunReport           # global per-round records (rank 0's copy)
+    bounds: list                # owned ranges
+    rank_records: list          # per-rank record arrays (all equal)
+    seconds: float
+
+
+# --------------------------------------------------------------------------
+# P ranks in one process on one GPU (tests)
+# --------------------------------------------------------------------------
+class VirtualMesh:
+    """`world` ranks sharing the current GPU: one shared region, stream and
+    1/world of the resident CTAs per rank."""
+
+    def __init__(self, graph: DeviceCsr, world: int, *, timeout_ms: int = 20000,
+                 ctas_per_rank: int | None = None):
+        L = _lib.load()
+        dev = graph.device
+        n = graph.num_nodes
+        self.world = world
+        self.bounds = partition_bounds_device(graph.row_offsets, world)
+        sms, per_sm = ctypes.c_int(0), ctypes.c_int(0)
+        _lib.check(L.hc_device_info(ctypes.byref(sms), ctypes.byref(per_sm)))
+        cap = sms.value * per_sm.value
+        ctas = ctas_per_rank if ctas_per_rank is not None else max(1, cap // world)
+        if ctas * world > cap:
+            raise ValueError(f"{world} ranks x {ctas} CTAs exceed the {cap} resident CTAs")
+        self.regions = [torch.zeros(L.hc_mg_shared_bytes(n), dtype=torch.uint8, device=dev)
+                        for _ in range(world)]
+        ptrs = [r.data_ptr() for r in self.regions]
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
+        self.ranks = [RankSolver(graph, lo, hi, p, world, ptrs, ctas=ctas, timeout_ms=timeout_ms)
+                      for p, (lo, hi) in enumerate(self.bounds)]
+        torch.cuda.synchronize()
+
+    def solve(self, mode: str, thr_count: int):
+        cur = torch.cuda.current_stream()
+        for s in self.streams:
+            s.wait_stream(cur)
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
+        for s in self.streams:
+            s.wait_event(start)
+        for rk, s in zip(self.ranks, self.streams):
+            rk.launch(mode, thr_count, s)
+        rounds = [rk.wait(s) for rk, s in zip(self.ranks, self.streams)]
+        stop = torch.cuda.Event(enable_timing=True)
+        for s in self.streams:
+            cur.wait_stream(s)
+        stop.record(cur)
+        stop.synchronize()
+        return rounds, start.elapsed_time(stop) / 1e3
+
+
+def virtual_color_graph(graph: DeviceCsr, config: HybridConfig | None = None, world: int = 2, *,
+                        graph_name: str = "graph", timeout_ms: int = 20000,
+                        mesh: VirtualMesh | None = None) -> MgResult:
+    """The multi-GPU solve with `world` ranks sharing the current GPU."""
+    config = config or HybridConfig()
+    mesh = mesh or VirtualMesh(graph, world, timeout_ms=timeout_ms)
+    thr = threshold_count(config, graph.num_nodes)
+    rounds, secs = mesh.solve(config.mode, thr)
+    if len(set(rounds)) != 1:
+        raise RuntimeError(f"ranks disagree on the round count: {rounds}")
+    recs = [rk.records(rounds[0]) for rk in mesh.ranks]
+    colors = torch.cat([rk.colors[: rk.hi - rk.lo] for rk in mesh.ranks]).cpu().numpy()
+    return MgResult(colors, _report(graph_name, graph, config, recs[0], rounds[0], secs),
+                    mesh.bounds, recs, secs)
+
+
+# --------------------------------------------------------------------------
+# one process per GPU (torch.distributed group; NVLink peer mappings)
+# --------------------------------------------------------------------------
+class PeerGroup:
+    """This rank's shared region plus every peer's, mapped into this process
+    through cudaIpc handles exchanged over the torch.distributed group."""
+
+    def __init__(self, num_nodes: int, group=None):
+        import torch.distributed as dist
+
+        self.L = L = _lib.load()
+        dev = _lib.device()
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        if self.world > MAX_WORLD:
+            raise ValueError(f"world size {self.world} > {MAX_WORLD}")
+        self.region = torch.zeros(L.hc_mg_shared_bytes(num_nodes), dtype=torch.uint8, device=dev)
+        torch.cuda.synchronize()
+        handle = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+        off = ctypes.c_int64(0)
+        _lib.check(L.hc_mg_ipc_export(self.region.data_ptr(), handle, ctypes.byref(off)))
+        mine = (bytes(handle.raw), int(off.value))
+        allinfo = [None] * self.world
+        dist.all_gather_object(allinfo, mine, group=group)
+        self.ptrs, self._opened = [], []
+        for q, (h, o) in enumerate(allinfo):
+            if q == self.rank:
+                self.ptrs.append(self.region.data_ptr())
+                continue
+            p = ctypes.c_void_p(0)
+            _lib.check(L.hc_mg_ipc_import(ctypes.create_string_buffer(h, IPC_HANDLE_BYTES), o, ctypes.byref(p)))
+            self.ptrs.append(int(p.value))
+            self._opened.append((int(p.value), o))
+        dist.barrier(group=group)
+
+    def close(self):
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)  # no peer still writes into a mapping
+        for p, o in self._opened:
+            _lib.check(self.L.hc_mg_ipc_close(ctypes.c_void_p(p), o))
+        self._opened = []
+
+
+class MgSolver:
+    """Reusable per-rank multi-GPU solve of one graph (every rank holds the
+    whole CSR; each processes only its owned rows)."""
+
+    def __init__(self, graph: DeviceCsr, group=None, *, timeout_ms: int = 60000):
+        self.g = graph
+        self.peers = PeerGroup(graph.num_nodes, group)
+        self.group = group
+        self.world, self.rank = self.peers.world, self.peers.rank
+        self.bounds = partition_bounds_device(graph.row_offsets, self.world)
+        lo, hi = self.bounds[self.rank]
+        self.rs = RankSolver(graph, lo, hi, self.rank, self.world, self.peers.ptrs, timeout_ms=timeout_ms)
+        self.mx = max(h - l for l, h in self.bounds)
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.stop = torch.cuda.Event(enable_timing=True)
+
+    def run(self, mode: str, thr_count: int) -> tuple[int, float]:
+        st = torch.cuda.current_stream()
+        self.start.record(st)
+        self.rs.launch(mode, thr_count, st)
+        self.stop.record(st)
+        rounds = self.rs.wait(st)
+        return rounds, self.start.elapsed_time(self.stop) / 1e3
+
+    def gather_colors(self) -> torch.Tensor:
+        import torch.distributed as dist
+
+        rs = self.rs
+        # gloo (tests: several processes on one GPU) gathers host tensors
+        dev = torch.device("cpu") if dist.get_backend(self.group) == "gloo" else rs.colors.device
+        buf = torch.zeros(max(self.mx, 1), dtype=torch.int64, device=dev)
+        buf[: rs.hi - rs.lo] = rs.colors[: rs.hi - rs.lo].to(dev)
+        out = torch.empty(self.world * buf.numel(), dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(out, buf, group=self.group)
+        out = out.view(self.world, -1)
+        return torch.cat([out[p, : hi - lo] for p, (lo, hi) in enumerate(self.bounds)])
+
+    def close(self):
+        self.peers.close()
+
+
+def mg_color_graph(graph: DeviceCsr, config: HybridConfig | None = None, *, group=None,
+                   graph_name: str = "graph", solver: MgSolver | None = None) -> MgResult:
+    """Partitioned solve of the whole graph, one process per GPU.  Returns the
+    whole coloring and the global RunReport on every rank."""
+    config = config or HybridConfig()
+    own = solver is None
+    solver = solver or MgSolver(graph, group)
+    try:
+        rounds, secs = solver.run(config.mode, threshold_count(config, graph.num_nodes))
+        recs = solver.rs.records(rounds)
+        colors = solver.gather_colors().cpu().numpy()
+    finally:
+        if own:
+            solver.close()
+    rep = _report(graph_name, graph, config, recs, rounds, secs)
+    rep.colors_used = int(colors.max()) if colors.size else 0
+    return MgResult(colors, rep, solver.bounds, [recs], secs)

@@ -1,0 +1,184 @@
+"""Device-resident multi-GPU solve over peer memory (hc_mg_*).
+
+One B200 is available per test box, so the P ranks share it:
+  * virtual ranks -- one process, P streams, P persistent kernels each on a
+    1/P share of the SMs, the shared regions as plain device pointers.  Same
+    kernel, mirrored stores, cross-GPU barrier + mailbox all-reduce as on P
+    GPUs;
+  * two processes on cuda:0 -- the cudaIpc export / import path that
+    one-process-per-GPU uses (kernels time-slice between the contexts).
+Everything must equal the single-GPU solve and the reference goldens
+bit-for-bit: colors, round count and every per-round (mode, wl_in, wl_out,
+conflicts).
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import MODES, THRESHOLDS
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+import paper_1912_01478_b200 as hc  # noqa: E402
+from paper_1912_01478_b200 import _lib  # noqa: E402
+from paper_1912_01478_b200 import graph as G  # noqa: E402
+from paper_1912_01478_b200.distributed import partition_bounds  # noqa: E402
+from paper_1912_01478_b200.multigpu import (VirtualMesh, partition_bounds_device,  # noqa: E402
+                                            virtual_color_graph)
+
+
+def _recs4(report):
+    return np.array([[int(r.mode_used == "topo"), r.worklist_size_in, r.worklist_size_out, r.conflicts]
+                     for r in report.per_round], dtype=np.int64).reshape(-1, 4)
+
+
+def _dev(ro, ci):
+    return hc.CsrGraph(len(ro) - 1, len(ci), ro, ci).to_device()
+
+
+def _check(dg, world, mode, thr, want_colors=None, want_recs=None):
+    cfg = hc.HybridConfig(mode=mode, threshold_fraction=thr)
+    if want_colors is None:
+        want_colors, rep1 = hc.color_graph(dg, cfg)
+        want_recs = _recs4(rep1)
+    res = virtual_color_graph(dg, cfg, world)
+    assert np.array_equal(res.colors, want_colors), (world, mode, thr)
+    assert np.array_equal(_recs4(res.report), want_recs), (world, mode, thr)
+    for r in res.rank_records[1:]:  # every rank holds the same global records
+        assert np.array_equal(r[:, :5], res.rank_records[0][:, :5])
+    return res
+
+
+def test_partition_bounds_device_matches_host():
+    for n, m in ((50, 300), (1000, 9000), (7, 0)):
+        ro, _ = O.build_csr(n, np.random.default_rng(n).integers(0, n, (m, 2))) if m else \
+            (np.zeros(n + 1, np.int64), None)
+        for w in (1, 2, 3, 4, 8):
+            assert partition_bounds_device(torch.from_numpy(ro).cuda(), w) == partition_bounds(ro, w)
+
+
+def test_virtual_ranks_match_reference_corpus(corpus):
+    """A slice of the reference's seeded corpora, P = 2 and 3 ranks, every
+    mode, two thresholds: colors + records equal the reference goldens."""
+    for i, g in enumerate(corpus[::7]):
+        if g.n < 2:
+            continue
+        dg = _dev(g.ro, g.ci)
+        world = 2 + (i % 2)
+        for mode in MODES:
+            for thr in (THRESHOLDS[0], THRESHOLDS[2]):
+                _check(dg, world, mode, thr, g.colors, g.records[(mode, thr)])
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_virtual_ranks_synthetic(world):
+    graphs = [
+        G.build_csr_device(G.gen_rmat_edges(12, 16, 1), 1 << 12),      # hubs, skew
+        G.build_csr_device(G.gen_er_edges(5000, 5000 * 16, 3), 5000),   # uniform
+        G.grid_graph(64, 48),                                            # delta columns
+    ]
+    for dg in graphs:
+        for mode in MODES:
+            _check(dg, world, mode, 0.6)
+
+
+def test_virtual_ranks_hub_graph_and_formats():
+    """32-bit state words (max degree > 16384), int64 offsets, and the
+    absolute-column format, each forced, on a graph with a split-hub regime."""
+    rng = np.random.default_rng(5)
+    n = 40000
+    hub = np.column_stack([np.zeros(20000, np.int64), rng.integers(1, n, 20000)])
+    rest = rng.integers(0, n, (60000, 2))
+    ro, ci = O.build_csr(n, np.vstack([hub, rest]))
+    dg = _dev(ro, ci)
+    want, rep = hc.color_graph(dg)
+    try:
+        for fmt in ((0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1)):
+            _lib.load().hc_solve_set_formats(*fmt)
+            res = virtual_color_graph(dg, hc.HybridConfig(), 3)
+            assert np.array_equal(res.colors, want), fmt
+            assert np.array_equal(_recs4(res.report), _recs4(rep)), fmt
+    finally:
+        _lib.load().hc_solve_set_formats(0, 0, 0)
+
+
+def test_virtual_ranks_repeated_solves_and_empty_ranges():
+    # barrier epochs continue across solves on the same mesh
+    dg = G.build_csr_device(G.gen_rmat_edges(10, 16, 4), 1 << 10)
+    want, rep = hc.color_graph(dg)
+    mesh = VirtualMesh(dg, 3)
+    for mode in ("hybrid", "data", "topo", "hybrid"):
+        res = virtual_color_graph(dg, hc.HybridConfig(mode=mode), 3, mesh=mesh)
+        w, r = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+        assert np.array_equal(res.colors, w) and np.array_equal(_recs4(res.report), _recs4(r))
+    # more ranks than nodes with edges: some ranks own nothing
+    k3 = _dev(np.array([0, 2, 4, 6]), np.array([1, 2, 0, 2, 0, 1]))
+    res = virtual_color_graph(k3, hc.HybridConfig(), 4)
+    assert res.colors.tolist() == [1, 2, 3] and res.report.total_rounds == 3
+
+
+def test_virtual_ranks_grid_closed_form():
+    r, c = 256, 200
+    res = virtual_color_graph(G.grid_graph(r, c), hc.HybridConfig(), 4)
+    i, j = np.divmod(np.arange(r * c), c)
+    assert np.array_equal(res.colors, 1 + (i + j) % 2)
+    assert res.report.total_rounds == (r + c + 1) // 2
+
+
+# ---------------------------------------------------------------- two processes
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _ipc_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1912_01478_b200.multigpu import MgSolver, mg_color_graph
+
+        dg = G.build_csr_device(G.gen_rmat_edges(8, 8, 2), 1 << 8)
+        solver = MgSolver(dg, timeout_ms=60000)
+        out = []
+        for mode in ("hybrid", "data"):
+            res = mg_color_graph(dg, hc.HybridConfig(mode=mode), solver=solver)
+            out.append((mode, res.colors, _recs4(res.report)))
+        solver.close()
+        q.put((rank, out, None))
+    except Exception as exc:  # reported to the parent
+        q.put((rank, None, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_ipc_share_one_gpu():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        rank, out, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}: {err}"
+        got[rank] = out
+    for p in procs:
+        p.join(timeout=60)
+    dg = G.build_csr_device(G.gen_rmat_edges(8, 8, 2), 1 << 8)
+    for mode, colors, recs in got[0]:
+        want, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+        assert np.array_equal(colors, want) and np.array_equal(recs, _recs4(rep)), mode
+    for a, b in zip(got[0], got[1]):
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
