@@ -76,6 +76,29 @@ def algorithmic_bytes(records: np.ndarray, stats: np.ndarray, n: int) -> int:
     return total
 
 
+def measured_traffic(config):
+    """DRAM bytes (read + write) of one solve_kernel launch of this config from
+    the committed ncu capture (profiles/r01_<config>_traffic.csv, written by
+    scripts/gpu_round.sh: dram__bytes_read.sum + dram__bytes_write.sum,
+    --clock-control none), or None when there is no capture."""
+    import csv
+
+    p = REPO / "profiles" / f"r01_{config}_traffic.csv"
+    if not p.exists():
+        return None
+    per_launch = {}
+    with p.open() as f:
+        for row in csv.DictReader(ln for ln in f if ln.startswith('"')):
+            if "solve_kernel" not in row.get("Kernel Name", ""):
+                continue
+            if row["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                key = row["ID"]
+                per_launch[key] = per_launch.get(key, 0) + int(float(row["Metric Value"].replace(",", "")))
+    if not per_launch:
+        return None
+    return int(sum(per_launch.values()) / len(per_launch))
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
 
@@ -268,45 +291,85 @@ def build_graph(hc, cfg):
 
 
 def run_distributed(args, cfg):
-    """N > 1: the 1D-partitioned solve (paper_1912_01478_b200.distributed) over
-    NCCL, one rank per GPU, the same graph on every rank (strong scaling)."""
+    """N > 1: one rank per GPU, 1D edge-balanced vertex partition of the same
+    graph (strong scaling).  The product path is the device-resident
+    peer-memory solve (multigpu.MgSolver: one persistent kernel per GPU,
+    boundary words stored into the peers' replicas over NVLink, cross-GPU
+    mailbox barriers); if the peer mapping is refused on this box, every rank
+    falls back to the NCCL per-phase exchange (distributed.dist_color_graph)
+    and the line says so."""
     import torch
     import torch.distributed as dist
 
     import paper_1912_01478_b200 as hc
     from paper_1912_01478_b200.distributed import dist_color_graph
+    from paper_1912_01478_b200.multigpu import MgSolver
 
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.share_gpu:  # test knob: every rank on cuda:0 (gloo; kernels time-slice)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if args.share_gpu:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     dg = build_graph(hc, cfg)
     n, und = dg.num_nodes, dg.num_undirected_edges
     hcfg = hc.HybridConfig(mode=args.mode)
+    thr = hc.threshold_count(hcfg, n)
     ro_host = dg.row_offsets.cpu().numpy()
+    try:
+        solver = MgSolver(dg)
+        exchange = ("peer memory: boundary state words stored into every peer's replica by the solve kernel "
+                    "(NVLink), cross-GPU mailbox barriers + (|W|, conflicts) all-reduce; one persistent kernel "
+                    "per GPU")
+    except Exception as exc:
+        solver = None
+        exchange = f"NCCL all-gather per phase (peer mapping unavailable: {exc!r})"
+
+    def step(graph=dg, ro=ro_host, slv=None):
+        slv = slv or solver
+        if slv is not None:
+            rounds, _ = slv.run(args.mode, thr)
+            return rounds
+        return dist_color_graph(graph.row_offsets, graph.col_indices, n, hcfg,
+                                host_row_offsets=ro).report.total_rounds
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
-        dist_color_graph(dg.row_offsets, dg.col_indices, n, hcfg, host_row_offsets=ro_host)
+        step()
     stream = torch.cuda.current_stream()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    dist.barrier()
+    rounds = 0
     torch.cuda.synchronize()
-    res = None
+    dist.barrier()
     with Clocks(local) as clk:
         for i in range(args.steps):
+            flush.zero_()  # L2 flush between timed steps, outside the events
             starts[i].record(stream)
-            res = dist_color_graph(dg.row_offsets, dg.col_indices, n, hcfg, host_row_offsets=ro_host)
+            rounds = step()
             stops[i].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
-    total_ms = float(sum(a.elapsed_time(b) for a, b in zip(starts, stops)))
-    t = torch.tensor([total_ms], device=dev)
+    step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
+    cdev = torch.device("cpu") if args.share_gpu else dev
+    t = torch.tensor([float(sum(step_ms))], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     value = und * args.steps / (total_ms / 1e3)
-    # e2e: host CSR (pinned) uploaded by every rank inside the timed region
+
+    # correctness of the timed path: global coloring valid, same on every rank
+    colors = solver.gather_colors() if solver is not None else None
+    valid = None
+    if colors is not None:
+        valid = hc.verify_coloring(dg, colors) == 0
+
+    # e2e: host CSR (pinned) uploaded by every rank, solve, colors gathered and
+    # copied back, inside the timed region
     host = hc.CsrGraph.pinned(dg.to_host())
     e2e_total = 0.0
     for i in range(args.warmup + args.steps):
@@ -314,12 +377,19 @@ def run_distributed(args, cfg):
         dist.barrier()
         t0 = time.perf_counter()
         d2 = host.to_device(dev)
-        r2 = dist_color_graph(d2.row_offsets, d2.col_indices, n, hcfg, host_row_offsets=ro_host)
+        if solver is not None:
+            # the peer mapping is made once (as a long-lived server would);
+            # the freshly uploaded CSR replaces the resident one
+            solver.g = solver.rs.g = d2
+            solver.run(args.mode, thr)
+            solver.gather_colors().cpu()
+        else:
+            dist_color_graph(d2.row_offsets, d2.col_indices, n, hcfg, host_row_offsets=ro_host)
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_total += (time.perf_counter() - t0) * 1e3
         del d2
-    t = torch.tensor([e2e_total], device=dev)
+    t = torch.tensor([e2e_total], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_total = float(t.item())
     if rank == 0:
@@ -329,17 +399,19 @@ def run_distributed(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPU",
             "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": args.mode,
-                       "num_nodes": n, "num_undirected_edges": und, "rounds": res.report.total_rounds,
-                       "parallelism": f"1d-partition x{world} (edge-balanced), NCCL exchange of boundary "
-                                      f"updates per phase", "exchanged_pairs": res.exchanged_pairs,
-                       "l2": "inputs > L2 per rank not guaranteed; no flush between steps"},
+                       "num_nodes": n, "num_undirected_edges": und, "rounds": rounds,
+                       "parallelism": f"1d-partition x{world} (edge-balanced)", "exchange": exchange,
+                       "valid": valid, "l2": "flushed between timed steps (512 MiB write)"},
             "clocks": clk.summary(),
-            "gpu_launches": (4 * res.report.total_rounds + 3) * args.steps,
+            "gpu_launches": (9 if solver is not None else 4 * rounds + 3) * args.steps,
             "e2e": {"value": und * args.steps / (e2e_total / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": world * (8 * (n + 1) + 8 * dg.num_edges),
                     "d2h_bytes_per_step": world * 8 * n},
+            "step_ms": step_ms,
         }
         print(json.dumps(line), flush=True)
+    if solver is not None:
+        solver.close()
     dist.destroy_process_group()
     return 0
 
@@ -442,7 +514,7 @@ def run_ours(args, cfg):
                    "sum_wl_in": sum_visits, "l2": "flushed between timed steps (512 MiB write)",
                    "parallelism": "single-gpu"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / hbm, "traffic": measured_traffic(args.config), "peak_kind": peak_kind,
                      "kernel": "solve_kernel (+ bin preprocessing, whole hc_solve step)",
                      "algorithmic_bytes_per_launch": b_alg},
         "clocks": clocks,
@@ -476,6 +548,8 @@ def main():
     ap.add_argument("--skip-modes", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N>1 test knob: all ranks on cuda:0 over gloo (correctness only, not a bench)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps

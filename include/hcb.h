@@ -180,6 +180,14 @@ int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int6
                 int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
                 int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
                 int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
+/* hc_mg_solve == hc_mg_prepare + hc_mg_launch.  Ranks sharing one GPU
+ * prepare all ranks first, then launch all (preprocessing kernels must not
+ * queue behind another rank's persistent kernel). */
+int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                  int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                  int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                  int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
+int hc_mg_launch(void *d_ws, void *stream);
 int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream);
 
 /* ------------------------------------------------------------------ */

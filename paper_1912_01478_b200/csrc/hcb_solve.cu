@@ -58,6 +58,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 
 #include "hcb_partition.cuh"
 
@@ -1159,6 +1161,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         const unsigned long long s = sm.red;
         __syncthreads();
         if (s == 0) break;  // worklist drained (driver.py:145)
+        if (F::mg && blockIdx.x == 0 && threadIdx.x == 0) C->rounds = t;  // progress (timeout report)
         if (rc.hub_split) {  // CTA-uniform: equal-size edge slices over the active hubs
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
             unsigned long long e_loc = 0;
@@ -1445,6 +1448,15 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
 // the multi-GPU shared region of a rank: state-word replica, then mailbox
 inline size_t mg_x_bytes(long long n) { return align_up(4 * (size_t)std::max(n, 1LL), 256); }
 
+// prepared multi-GPU launches, keyed by workspace (hc_mg_prepare -> hc_mg_launch)
+struct MgLaunch {
+    Params P;
+    const void *fn;
+    bool regular;
+};
+static std::mutex g_mg_mu;
+static std::unordered_map<void *, MgLaunch> g_mg_prepared;
+
 // driver API entry point (no -lcuda link: the library must load without a GPU)
 typedef int (*MemGetAddressRangeFn)(unsigned long long *, size_t *, unsigned long long);
 static MemGetAddressRangeFn mem_get_address_range() {
@@ -1608,10 +1620,10 @@ int hc_mg_ipc_close(void *d_ptr, int64_t offset) {
     return HC_OK;
 }
 
-int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
-                int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
-                int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
-                int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
+int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                  int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                  int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                  int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
     HC_REQUIRE(num_nodes >= 1 && num_nodes < 0x7fffffffLL, HC_ERR_INVALID,
                "hc_mg_solve: num_nodes %lld out of range", (long long)num_nodes);
     HC_REQUIRE(num_edges >= 0, HC_ERR_INVALID, "hc_mg_solve: num_edges < 0");
@@ -1670,12 +1682,36 @@ int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int6
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_mg_solve: occupancy query failed");
     const unsigned full = (unsigned)(per_sm * std::max(1, num_sms()));
     P.nblocks = ctas > 0 ? std::min((unsigned)ctas, full) : full;
-    void *args[] = {&P};
-    if (ctas > 0)  // caller-sized grid (several ranks sharing one GPU): regular launch
-        HC_CUDA_TRY(cudaLaunchKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
+    std::lock_guard<std::mutex> lk(g_mg_mu);
+    g_mg_prepared[d_ws] = MgLaunch{P, fn, ctas > 0};
+    return HC_OK;
+}
+
+int hc_mg_launch(void *d_ws, void *stream) {
+    MgLaunch L;
+    {
+        std::lock_guard<std::mutex> lk(g_mg_mu);
+        auto it = g_mg_prepared.find(d_ws);
+        HC_REQUIRE(it != g_mg_prepared.end(), HC_ERR_INVALID, "hc_mg_launch: workspace not prepared");
+        L = it->second;
+    }
+    cudaStream_t st = as_stream(stream);
+    void *args[] = {&L.P};
+    if (L.regular)  // caller-sized grid (several ranks sharing one GPU): regular launch
+        HC_CUDA_TRY(cudaLaunchKernel(L.fn, dim3(L.P.nblocks), dim3(BLOCK), args, 0, st));
     else
-        HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
+        HC_CUDA_TRY(cudaLaunchCooperativeKernel(L.fn, dim3(L.P.nblocks), dim3(BLOCK), args, 0, st));
     return HC_OK;  // asynchronous: hc_mg_wait collects the outcome
+}
+
+int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
+    const int rc = hc_mg_prepare(d_row_offsets, d_col_indices, num_nodes, num_edges, lo, hi, rank, world,
+                                 h_shared, mode, thr_count, d_colors, d_rec, max_rec, ctas, timeout_ms, d_ws,
+                                 ws_bytes, stream);
+    return rc != HC_OK ? rc : hc_mg_launch(d_ws, stream);
 }
 
 int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream) {
@@ -1689,7 +1725,9 @@ int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream) {
     HC_CUDA_TRY(cudaMemcpyAsync(&info, &C->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaMemcpyAsync(&abort, &C->abort, sizeof abort, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
-    HC_REQUIRE(!abort, HC_ERR_TIMEOUT, "hc_mg_solve: a peer did not reach a cross-GPU barrier in time");
+    HC_REQUIRE(!abort, HC_ERR_TIMEOUT,
+               "hc_mg_solve: a peer did not reach a cross-GPU barrier in time (this rank in round %lld)",
+               info.rounds);
     if (h_rounds) *h_rounds = info.rounds;
     HC_REQUIRE(!info.rec_overflow, HC_ERR_RECORDS, "hc_mg_solve: %lld rounds exceed the record buffer",
                info.rounds);

@@ -87,8 +87,13 @@ class RankSolver:
         self.timeout_ms = int(timeout_ms)
 
     def launch(self, mode: str, thr_count: int, stream: torch.cuda.Stream | None = None) -> None:
+        self.prepare(mode, thr_count, stream)
+        _lib.check(self.L.hc_mg_launch(self.ws.data_ptr(), _lib.stream_handle(stream)))
+
+    def prepare(self, mode: str, thr_count: int, stream: torch.cuda.Stream | None = None) -> None:
+        """Preprocessing of the owned range (synchronous); hc_mg_launch starts the solve."""
         g = self.g
-        _lib.check(self.L.hc_mg_solve(
+        _lib.check(self.L.hc_mg_prepare(
             g.row_offsets.data_ptr(), _lib.ptr(g.col_indices), g.num_nodes, g.num_edges,
             self.lo, self.hi, self.rank, self.world, ctypes.cast(self.shared, ctypes.c_void_p),
             _lib.MODE_CODES[mode], int(thr_count),
@@ -160,8 +165,12 @@ class VirtualMesh:
         start.record(cur)
         for s in self.streams:
             s.wait_event(start)
+        # preprocessing of every rank first: no rank's preprocessing kernels
+        # may queue behind another rank's persistent kernel on the shared GPU
         for rk, s in zip(self.ranks, self.streams):
-            rk.launch(mode, thr_count, s)
+            rk.prepare(mode, thr_count, s)
+        for rk, s in zip(self.ranks, self.streams):
+            _lib.check(rk.L.hc_mg_launch(rk.ws.data_ptr(), _lib.stream_handle(s)))
         rounds = [rk.wait(s) for rk, s in zip(self.ranks, self.streams)]
         stop = torch.cuda.Event(enable_timing=True)
         for s in self.streams:
@@ -213,15 +222,27 @@ class PeerGroup:
         allinfo = [None] * self.world
         dist.all_gather_object(allinfo, mine, group=group)
         self.ptrs, self._opened = [], []
-        for q, (h, o) in enumerate(allinfo):
-            if q == self.rank:
-                self.ptrs.append(self.region.data_ptr())
-                continue
-            p = ctypes.c_void_p(0)
-            _lib.check(L.hc_mg_ipc_import(ctypes.create_string_buffer(h, IPC_HANDLE_BYTES), o, ctypes.byref(p)))
-            self.ptrs.append(int(p.value))
-            self._opened.append((int(p.value), o))
-        dist.barrier(group=group)
+        err = None
+        try:
+            for q, (h, o) in enumerate(allinfo):
+                if q == self.rank:
+                    self.ptrs.append(self.region.data_ptr())
+                    continue
+                p = ctypes.c_void_p(0)
+                _lib.check(L.hc_mg_ipc_import(ctypes.create_string_buffer(h, IPC_HANDLE_BYTES), o,
+                                              ctypes.byref(p)))
+                self.ptrs.append(int(p.value))
+                self._opened.append((int(p.value), o))
+        except Exception as exc:  # every rank must learn that the mapping failed somewhere
+            err = exc
+        flags = [None] * self.world
+        dist.all_gather_object(flags, err is None, group=group)
+        if not all(flags):
+            for p, o in self._opened:
+                L.hc_mg_ipc_close(ctypes.c_void_p(p), o)
+            self._opened = []
+            raise RuntimeError(f"peer mapping failed on ranks {[q for q, f in enumerate(flags) if not f]}: "
+                               f"{err!r}")
 
     def close(self):
         import torch.distributed as dist
