@@ -250,6 +250,29 @@ int hc_verify(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_
 /* d_acc: int64[2] device scratch */
 int hc_colors_used(const int64_t *d_colors, int64_t num_nodes, int64_t *d_acc, int64_t *h_used,
                    void *stream);
+/* MatrixMarket coordinate entries (graph.py:105-181) parsed on the device.
+ * d_bytes = the file content AFTER the size line (the host parses banner and
+ * size line); universal_newlines: '\r' also ends a line (files read in text
+ * mode).  Entry k (k-th non-blank, non-comment line) -> d_edges[2k..2k+1] =
+ * (row-1, col-1), int64[2*nnz].  On return *h_num_entries = entry lines; if
+ * some line is bad, *h_err_line / *h_err_code / h_err_span[2] (byte span)
+ * name the FIRST bad line (the reference raises there), else *h_err_line=-1.
+ * *h_first_nonascii = offset of the first byte >= 0x80 or -1. */
+#define HC_MTX_FEW_FIELDS 1  /* "entry needs at least two coordinates" */
+#define HC_MTX_NON_INTEGER 2 /* "non-integer coordinate"               */
+#define HC_MTX_BOUNDS 3      /* "coordinate (r, c) outside declared bounds" */
+#define HC_MTX_TOO_MANY 4    /* "more than the declared nnz entries"   */
+size_t hc_mtx_workspace_bytes(int64_t num_bytes);
+int hc_mtx_parse(const uint8_t *d_bytes, int64_t num_bytes, int universal_newlines, int64_t rows, int64_t cols,
+                 int64_t nnz, int64_t *d_edges, int64_t *h_num_entries, int64_t *h_err_line, int *h_err_code,
+                 int64_t *h_err_span, int64_t *h_first_nonascii, void *d_ws, size_t ws_bytes, void *stream);
+
+/* degree_stats (graph.py:204-217): min, max and the element at sorted index
+ * n/2 (np.partition) of the degree array, on the device (radix select). */
+size_t hc_degree_stats_workspace_bytes(void);
+int hc_degree_stats(const int64_t *d_row_offsets, int64_t num_nodes, int64_t *h_min, int64_t *h_median,
+                    int64_t *h_max, void *d_ws, size_t ws_bytes, void *stream);
+
 /* int64 -> int32 column conversion for uploads of reference CsrGraph arrays */
 int hc_narrow_i64_i32(const int64_t *d_in, int32_t *d_out, int64_t count, void *stream);
 

@@ -37,6 +37,26 @@ from .graph import (
     rmat_graph,
     synthetic,
 )
+from .ingest import (
+    DegreeStats,
+    MatrixMarketError,
+    degree_stats,
+    load_csr_cache,
+    load_graph,
+    load_graph_device,
+    parse_matrix_market,
+    save_csr_cache,
+)
+from .pushbench import (
+    BenchConfig,
+    TtiRecord,
+    TtiSeries,
+    collect_deactivations,
+    detect_crossovers,
+    expected_iterations,
+    run_push_bench,
+    write_tti_csv,
+)
 from .worklist import Worklist, init_full
 
 __version__ = "0.1.0"
@@ -49,6 +69,10 @@ __all__ = [
     "CsrGraph", "DeviceCsr", "EdgeList", "build_csr", "build_csr_device",
     "er_graph", "gen_er_edges", "gen_grid_edges", "gen_rmat_edges", "grid_graph",
     "rmat_graph", "synthetic",
+    "DegreeStats", "MatrixMarketError", "degree_stats", "load_csr_cache", "load_graph",
+    "load_graph_device", "parse_matrix_market", "save_csr_cache",
+    "BenchConfig", "TtiRecord", "TtiSeries", "collect_deactivations", "detect_crossovers",
+    "expected_iterations", "run_push_bench", "write_tti_csv",
     "Worklist", "init_full",
     "__version__",
 ]

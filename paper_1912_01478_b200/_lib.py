@@ -102,6 +102,11 @@ _SIGS = {
     "hc_verify": (ctypes.c_int, [_p, _p, _i64, _p, _p, _p, _p]),
     "hc_colors_used": (ctypes.c_int, [_p, _i64, _p, _p, _p]),
     "hc_narrow_i64_i32": (ctypes.c_int, [_p, _p, _i64, _p]),
+    "hc_mtx_workspace_bytes": (ctypes.c_size_t, [_i64]),
+    "hc_mtx_parse": (ctypes.c_int, [_p, _i64, ctypes.c_int, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p,
+                                    ctypes.c_size_t, _p]),
+    "hc_degree_stats_workspace_bytes": (ctypes.c_size_t, []),
+    "hc_degree_stats": (ctypes.c_int, [_p, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -273,6 +273,10 @@ __device__ __forceinline__ void seg_put(const Params &P, int np, int bin, unsign
     }
 }
 
+// set by any thread of the CTA that issued NVLink stores in the current
+// phase: only such CTAs need the system-scope fence before the next barrier
+__shared__ unsigned s_mirrored;
+
 // Cross-GPU barrier of the multi-GPU solve: the grid barrier whose last
 // arriving CTA exchanges (epoch, payload) with every rank's mailbox over
 // NVLink.  kind 0: plain;  kind 1: end of round t with parity p -- payload =
@@ -287,7 +291,12 @@ __device__ bool mg_sync(const Params &P, Smem &sm, unsigned long long epoch, int
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned g = ld_acquire_u32(&b->gen);
-        __threadfence_system();
+        if (s_mirrored) {  // this CTA's NVLink stores reach the peers before the arrival
+            __threadfence_system();
+            s_mirrored = 0u;
+        } else {
+            __threadfence();
+        }
         const unsigned arrived = atomicAdd(&b->count, 1u);
         if (arrived == P.nblocks - 1) {
             atomicExch(&b->count, 0u);
@@ -380,6 +389,7 @@ __device__ __forceinline__ void xraw(const Params &P, long long v, unsigned w) {
 // cross-GPU barrier).  Interior words are read by no other rank.
 template <class F>
 __device__ __noinline__ void mirror(const Params &P, long long v, unsigned w) {
+    s_mirrored = 1u;
     for (int q = 0; q < P.world; ++q)
         if (q != P.rank)
             reinterpret_cast<typename F::xt *>(__ldg(reinterpret_cast<const unsigned long long *>(P.peer_x) + q))[v] =
@@ -1040,6 +1050,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
     // every replica is zeroed before any peer mirrors into it
     unsigned long long ep = 0;
     if constexpr (F::mg) {
+        if (threadIdx.x == 0) s_mirrored = 0u;
         ep = *(volatile unsigned long long *)&P.mbox->last_epoch;
         if (!mg_sync(P, sm, ++ep, 0, 0)) return;
     } else {

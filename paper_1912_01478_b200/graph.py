@@ -8,8 +8,8 @@ plus the device-resident `DeviceCsr` (int64 row offsets, int32 column ids:
 SURVEY.md §8(a) a12) that the solver consumes, and the on-device synthetic
 generators of SURVEY.md Appendix C (hc_gen_grid / hc_gen_er / hc_gen_rmat).
 
-MatrixMarket parsing and the .npz cache (graph.py:105-181, 220-254) are host
-file formats off the solve path and stay out of scope.
+MatrixMarket ingestion (device parser), the .npz cache and degree_stats
+live in ingest.py (graph.py:96-254).
 """
 
 from __future__ import annotations
