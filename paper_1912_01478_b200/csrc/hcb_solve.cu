@@ -119,15 +119,17 @@ struct Ctrl {
 };
 
 // Multi-GPU mailbox, one per rank, in the rank's peer-mapped shared region
-// (after its state-word replica).  Rank r's cross-GPU barrier number e posts
-// (e, payload) into slot [e & 1][r] of every rank's mailbox (st.release.sys)
-// and waits until all slots [e & 1][*] of its own mailbox reach e.  Two slot
+// (after its state-word replica).  Rank r's cross-GPU barrier number e writes
+// three tagged words (e_lo32 << 32 | value32: |W'|, conflicts lo / hi) into
+// slot [e & 1][r] of every rank's mailbox and waits until every slot
+// [e & 1][*] of its own mailbox carries tag e.  Tagged words make each word
+// self-validating, so the post is ONE system fence + relaxed stores and the
+// wait is relaxed polls + ONE fence (no per-word release / acquire).  Two slot
 // sets suffice: a rank can post e+2 only after every rank posted e+1, i.e.
 // after every rank finished reading the payloads of e.
 constexpr int MG_MAX_WORLD = 8;
 struct MboxSlot {
-    unsigned long long epoch;
-    unsigned long long a, b;
+    unsigned long long w[3];
     unsigned long long pad;
 };
 struct Mbox {
@@ -285,14 +287,16 @@ __shared__ unsigned s_mirrored;
 // Every CTA fences its mirrored stores (fence.sc.sys) before arriving, so a
 // peer that passes the barrier sees them.  Returns false if some rank did not
 // arrive within P.timeout_ns (the whole grid then leaves the kernel).
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+
 __device__ bool mg_sync(const Params &P, Smem &sm, unsigned long long epoch, int kind, int p) {
     Ctrl *C = P.ctrl;
     GridBarrier *b = &C->bar;
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned g = ld_acquire_u32(&b->gen);
-        if (s_mirrored) {  // this CTA's NVLink stores reach the peers before the arrival
-            __threadfence_system();
+        if (s_mirrored) {  // this CTA's NVLink stores are ordered before its arrival
+            fence_acq_rel_sys();
             s_mirrored = 0u;
         } else {
             __threadfence();
@@ -300,34 +304,44 @@ __device__ bool mg_sync(const Params &P, Smem &sm, unsigned long long epoch, int
         const unsigned arrived = atomicAdd(&b->count, 1u);
         if (arrived == P.nblocks - 1) {
             atomicExch(&b->count, 0u);
-            __threadfence_system();
             unsigned long long a = 0, c = 0;
             if (kind == 1) {
                 a = __ldcg(&C->wl_next[p ^ 1]) + __ldcg(&C->hub_cnt[p ^ 1]);
                 c = __ldcg(&C->conflicts[p]);
             }
+            // release: everything this GPU wrote (observed through the
+            // arrivals) before the tags; then relaxed tagged stores
+            fence_acq_rel_sys();
+            const unsigned long long tag = (epoch & 0xffffffffull) << 32;
+            const unsigned long long wv[3] = {tag | (a & 0xffffffffull), tag | (c & 0xffffffffull), tag | (c >> 32)};
             const int par = (int)(epoch & 1ull);
             for (int q = 0; q < P.world; ++q) {
                 MboxSlot *sl = &P.peer_mbox[q]->slot[par][P.rank];
-                st_relaxed_sys_u64(&sl->a, a);
-                st_relaxed_sys_u64(&sl->b, c);
-                st_release_sys_u64(&sl->epoch, epoch);
+#pragma unroll
+                for (int w = 0; w < 3; ++w) st_relaxed_sys_u64(&sl->w[w], wv[w]);
             }
             const unsigned long long t0 = globaltimer();
             unsigned long long sa = 0, sc = 0;
             unsigned ok = 1;
             for (int q = 0; q < P.world && ok; ++q) {
                 MboxSlot *sl = &P.mbox->slot[par][q];
-                while (ld_acquire_sys_u64(&sl->epoch) < epoch) {
-                    if ((long long)(globaltimer() - t0) > P.timeout_ns) {
-                        ok = 0;
-                        break;
+#pragma unroll 1
+                for (int w = 0; w < 3 && ok; ++w) {
+                    unsigned long long v;
+                    while (((v = ld_relaxed_sys_u64(&sl->w[w])) & ~0xffffffffull) != tag) {
+                        if ((long long)(globaltimer() - t0) > P.timeout_ns) {
+                            ok = 0;
+                            break;
+                        }
+                        __nanosleep(20);
                     }
-                    __nanosleep(32);
+                    const unsigned long long val = v & 0xffffffffull;
+                    if (w == 0) sa += val;
+                    else if (w == 1) sc += val;
+                    else sc += val << 32;
                 }
-                sa += ld_relaxed_sys_u64(&sl->a);
-                sc += ld_relaxed_sys_u64(&sl->b);
             }
+            fence_acq_rel_sys();  // acquire: the peers' data before the tags they posted
             if (!ok) C->abort = 1u;
             if (kind == 1) {
                 C->g_wl = sa;
