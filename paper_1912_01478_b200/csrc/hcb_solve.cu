@@ -267,12 +267,13 @@ __device__ __forceinline__ void mark(unsigned *bm, unsigned c) {
 
 // loser count of output segment c of bin `bin`; the multi-GPU solve also
 // keeps this rank's next-worklist total for the cross-GPU reduction
+// (thread 0 of the CTA; the multi-GPU total is kept per CTA and added once
+// per round at the end of resolve)
+__shared__ unsigned long long s_wl_acc;
 template <bool MG>
 __device__ __forceinline__ void seg_put(const Params &P, int np, int bin, unsigned c, unsigned cnt) {
     P.ctrl->segcnt[np][bin][c] = cnt;
-    if constexpr (MG) {
-        if (cnt) atomicAdd(&P.ctrl->wl_next[np], (unsigned long long)cnt);
-    }
+    if constexpr (MG) s_wl_acc += cnt;
 }
 
 // set by any thread of the CTA that issued NVLink stores in the current
@@ -402,7 +403,7 @@ __device__ __forceinline__ void xraw(const Params &P, long long v, unsigned w) {
 // peer's replica (NVLink stores; made visible by the fence.sys of the next
 // cross-GPU barrier).  Interior words are read by no other rank.
 template <class F>
-__device__ __noinline__ void mirror(const Params &P, long long v, unsigned w) {
+__device__ __forceinline__ void mirror(const Params &P, long long v, unsigned w) {
     s_mirrored = 1u;
     for (int q = 0; q < P.world; ++q)
         if (q != P.rank)
@@ -1064,7 +1065,10 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
     // every replica is zeroed before any peer mirrors into it
     unsigned long long ep = 0;
     if constexpr (F::mg) {
-        if (threadIdx.x == 0) s_mirrored = 0u;
+        if (threadIdx.x == 0) {
+            s_mirrored = 0u;
+            s_wl_acc = 0ull;
+        }
         ep = *(volatile unsigned long long *)&P.mbox->last_epoch;
         if (!mg_sync(P, sm, ++ep, 0, 0)) return;
     } else {
@@ -1233,6 +1237,10 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
             if (lane == 0 && v) atomicAdd(&sm.red, v);
             __syncthreads();
             if (threadIdx.x == 0 && sm.red) atomicAdd(&C->conflicts[p], sm.red);
+            if (F::mg && threadIdx.x == 0 && s_wl_acc) {
+                atomicAdd(&C->wl_next[np], s_wl_acc);
+                s_wl_acc = 0ull;
+            }
             if (STATS) {
                 for (int q = 0; q < 2; ++q) {
                     const unsigned long long e = warp_sum(my_edges[q]);
