@@ -130,6 +130,10 @@ size_t hc_solve_workspace_bytes(int64_t num_nodes, int64_t num_edges);
  * force int64 row offsets, forbid 16-bit state words, forbid 16-bit delta
  * columns.  Defaults (0, 0, 0) let hc_solve pick per graph. */
 int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16);
+/* Graphs whose every degree is <= 16 (grids, meshes, road networks) run a
+ * bin-0-only instantiation (less shared memory, more resident CTAs);
+ * allow = 0 forces the general kernel (tests / experiments). */
+int hc_solve_set_small(int allow);
 int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
              int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
              hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, void *d_ws,

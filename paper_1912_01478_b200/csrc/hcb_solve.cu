@@ -80,8 +80,17 @@ constexpr int BLOCK = HC_BLOCK;
 #define HC_MINB (1024 / HC_BLOCK)
 #endif
 constexpr int MIN_CTAS = HC_MINB;        // resident CTAs per SM the register budget targets
+#ifndef HC_MINB_SMALL
+#define HC_MINB_SMALL 3
+#endif
+constexpr int MIN_CTAS_SMALL = HC_MINB_SMALL;  // the same for bin-0-only graphs (SmemT<true>)
 constexpr int NW = BLOCK / 32;
 constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
+#ifndef HC_NPT_SMALL
+#define HC_NPT_SMALL 2
+#endif
+constexpr int NPT_SMALL = HC_NPT_SMALL;  // the same in the bin-0-only kernel (more CTAs, fewer registers)
+static_assert(NPT_SMALL <= NPT, "shared tables are sized for NPT");
 constexpr int NSEG_BINS = 4;             // bins 0..3 are segmented; bin 4 (hubs) is dense
 constexpr int BIN_HUB = 4;
 constexpr int NBIN = 5;
@@ -200,12 +209,16 @@ struct RoundCfg {
     bool topo, ident, bin3_by_cta, ident_small;
 };
 
-struct Smem {
+// SMALL: the graph has only bin-0 nodes (max degree <= 16: grids, meshes,
+// road networks); the kernel then carries neither the group / hub code nor
+// their shared memory, so it fits more CTAs per SM with a larger L1.
+template <bool SMALL>
+struct SmemT {
     RoundCfg rc;
-    unsigned hub_pre[MAX_SPLIT_SLOTS + 1];    // slice prefix over the active hubs (split rounds)
-    unsigned prefix[NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
-    unsigned win_bm[NW][WIN_WORDS];
-    unsigned hub_bm[HUB_WORDS];
+    unsigned hub_pre[SMALL ? 1 : MAX_SPLIT_SLOTS + 1];    // slice prefix over the active hubs (split rounds)
+    unsigned prefix[SMALL ? 1 : NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
+    unsigned win_bm[SMALL ? 1 : NW][WIN_WORDS];
+    unsigned hub_bm[SMALL ? 1 : HUB_WORDS];
     unsigned warp_tmp[NPT * NW];
     unsigned cnt_tab[2][NPT * NW];
     unsigned long long red;
@@ -214,6 +227,7 @@ struct Smem {
     unsigned out_cnt;
     unsigned mg_abort;
 };
+using Smem = SmemT<false>;
 
 // dynamic list of parity p, bin b (selects instead of a runtime-indexed
 // kernel-parameter array, which would force a local-memory copy of Params)
@@ -290,7 +304,8 @@ __shared__ unsigned s_mirrored;
 // arrive within P.timeout_ns (the whole grid then leaves the kernel).
 __device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
-__device__ bool mg_sync(const Params &P, Smem &sm, unsigned long long epoch, int kind, int p) {
+template <class SMT>
+__device__ bool mg_sync(const Params &P, SMT &sm, unsigned long long epoch, int kind, int p) {
     Ctrl *C = P.ctrl;
     GridBarrier *b = &C->bar;
     __syncthreads();
@@ -368,11 +383,13 @@ __device__ bool mg_sync(const Params &P, Smem &sm, unsigned long long epoch, int
 // All solver logic works on the 32-bit encoding; the accessors convert.
 //   MG          multi-GPU (hc_mg_solve): this rank owns [lo, lo+nown); writes
 //               of owned boundary words are mirrored into every peer's replica
-template <typename XT, typename CT, bool MG = false>
+//   SMALL       only bin-0 nodes (see SmemT)
+template <typename XT, typename CT, bool MG = false, bool SMALL = false>
 struct Fmt {
     using xt = XT;
     using ct = CT;
     static constexpr bool mg = MG;
+    static constexpr bool small = SMALL;
 };
 using F32 = Fmt<unsigned, int>;
 using F16 = Fmt<unsigned short, int>;
@@ -382,6 +399,14 @@ using MF32 = Fmt<unsigned, int, true>;
 using MF16 = Fmt<unsigned short, int, true>;
 using MF16D = Fmt<unsigned short, short, true>;
 using MF32D = Fmt<unsigned, short, true>;
+using SF32 = Fmt<unsigned, int, false, true>;
+using SF16 = Fmt<unsigned short, int, false, true>;
+using SF16D = Fmt<unsigned short, short, false, true>;
+using SF32D = Fmt<unsigned, short, false, true>;
+using SMF32 = Fmt<unsigned, int, true, true>;
+using SMF16 = Fmt<unsigned short, int, true, true>;
+using SMF16D = Fmt<unsigned short, short, true, true>;
+using SMF32D = Fmt<unsigned, short, true, true>;
 
 // committed flag / color mask of the format's state word; words are kept
 // zero-extended in registers, so no conversion on load or store
@@ -643,19 +668,20 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
 }
 
 // ------------------------------------------------------------------ bin 0
-// Thread per node, NPT nodes per thread; all list / offset / first-four-
-// neighbour loads of the NPT nodes are issued before any is consumed.
+// Thread per node, NP nodes per thread (NPT, or NPT_SMALL in the bin-0-only kernel); all list / offset / first-four-
+// neighbour loads of the NP nodes are issued before any is consumed.
 template <typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
-                                           unsigned long long hi, int u[NPT], bool lost[NPT],
+                                           unsigned long long hi, int *u, bool *lost,
                                            unsigned long long &my_conf, unsigned long long *my_edges) {
+    constexpr int NP = F::small ? NPT_SMALL : NPT;
     const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
-    unsigned xu[NPT];
+    unsigned xu[NP];
     unsigned seg = ident ? 0u : list_segment(L, prefix, base);  // same for the whole CTA (broadcast)
 #pragma unroll
-    for (int j = 0; j < NPT; ++j) {
+    for (int j = 0; j < NP; ++j) {
         const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
         u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
         lost[j] = false;
@@ -663,34 +689,34 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
     }
     // the row offsets are loaded together with the activity word (speculative
     // for inactive nodes in topology sweeps): one dependent round trip less
-    OffT rb[NPT], re[NPT];
+    OffT rb[NP], re[NP];
 #pragma unroll
-    for (int j = 0; j < NPT; ++j) {
+    for (int j = 0; j < NP; ++j) {
         rb[j] = u[j] >= 0 ? ro[u[j]] : OffT(0);
         re[j] = u[j] >= 0 ? ro[u[j] + 1] : OffT(0);
     }
     if (topo || PHASE == 1) {
 #pragma unroll
-        for (int j = 0; j < NPT; ++j) xu[j] = u[j] >= 0 ? xget<F>(P, u[j]) : 0u;
+        for (int j = 0; j < NP; ++j) xu[j] = u[j] >= 0 ? xget<F>(P, u[j]) : 0u;
         if (topo) {
 #pragma unroll
-            for (int j = 0; j < NPT; ++j)
+            for (int j = 0; j < NP; ++j)
                 if (xu[j] & FB<F>) { u[j] = -1; re[j] = rb[j]; }  // inactive (_kernels.pyx:76-77, 135-136)
         }
     }
-    int nb[NPT][4];
+    int nb[NP][4];
 #pragma unroll
-    for (int j = 0; j < NPT; ++j)
+    for (int j = 0; j < NP; ++j)
 #pragma unroll
         for (int q = 0; q < 4; ++q) nb[j][q] = rb[j] + q < re[j] ? colget<F>(P, rb[j] + q, u[j]) : -1;
     if (PHASE == 0) {
-        unsigned x[NPT][4];
+        unsigned x[NP][4];
 #pragma unroll
-        for (int j = 0; j < NPT; ++j)
+        for (int j = 0; j < NP; ++j)
 #pragma unroll
             for (int q = 0; q < 4; ++q) x[j][q] = nb[j][q] >= 0 ? xget<F>(P, nb[j][q]) : 0u;
 #pragma unroll
-        for (int j = 0; j < NPT; ++j) {
+        for (int j = 0; j < NP; ++j) {
             if (u[j] < 0) continue;
             unsigned long long mask = 0;
 #pragma unroll
@@ -709,13 +735,13 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
             if (STATS) my_edges[0] += re[j] - rb[j];
         }
     } else {
-        unsigned x[NPT][4];
+        unsigned x[NP][4];
 #pragma unroll
-        for (int j = 0; j < NPT; ++j)
+        for (int j = 0; j < NP; ++j)
 #pragma unroll
             for (int q = 0; q < 4; ++q) x[j][q] = (nb[j][q] >= 0 && nb[j][q] < u[j]) ? xget<F>(P, nb[j][q]) : 0u;
 #pragma unroll
-        for (int j = 0; j < NPT; ++j) {
+        for (int j = 0; j < NP; ++j) {
             if (u[j] < 0) continue;
             const unsigned T = xu[j];
             unsigned cnt = 0, low = 0;
@@ -895,14 +921,67 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
     return total;
 }
 
+// A chunk of bin 0 (thread per node, NP nodes per thread per tile).
+template <typename OffT, class F, bool STATS, int PHASE, class SMT>
+__device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT &sm, unsigned c, int np,
+                                           unsigned long long &my_conf, unsigned long long *my_edges) {
+    constexpr int NP = F::small ? NPT_SMALL : NPT;
+    const RoundCfg &rc = sm.rc;
+    const unsigned csz0 = rc.csz[0];
+    const unsigned long long lo = (unsigned long long)c * csz0;
+    const unsigned long long hi = min(lo + csz0, rc.L[0].total);
+    int *out = dyn_list(P, np, 0) + (long long)c * csz0;
+    // order-preserving compaction of the losers (index order j-major, then
+    // thread), ONE barrier per tile: every warp publishes its per-j loser
+    // counts into a double-buffered table and scans it itself.  (Order only
+    // affects locality, but an unordered list fragments round after round.)
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    unsigned written = 0, buf = 0;
+    for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NP) {
+        int u[NP];
+        bool lost[NP];
+        small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
+        if (PHASE == 1) {
+            unsigned bal[NP];
+#pragma unroll
+            for (int j = 0; j < NP; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
+            if (lane < NP) {
+                unsigned mine = 0;
+#pragma unroll
+                for (int j = 0; j < NP; ++j)
+                    if (lane == (unsigned)j) mine = __popc(bal[j]);
+                sm.cnt_tab[buf][lane * NW + warp] = mine;
+            }
+            __syncthreads();
+            unsigned run = written;
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                const unsigned v = lane < NW ? sm.cnt_tab[buf][j * NW + lane] : 0u;
+                const unsigned incl = warp_incl_scan(v);
+                const unsigned before = __shfl_sync(FULL, incl - v, warp);  // warps < me in slice j
+                const unsigned tot_j = __shfl_sync(FULL, incl, 31);
+                if (lost[j]) out[run + before + __popc(bal[j] & lanemask_lt())] = u[j];
+                run += tot_j;
+            }
+            written = run;
+            buf ^= 1u;
+        }
+    }
+    if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 0, c, written);
+}
+
 // One unit of one phase.  All CTA-uniform inputs come from shared memory.
 // Unit ranges: [ubase0, ubase1) hubs, then bins 3, 2, 1, 0.
-template <typename OffT, class F, bool STATS, int PHASE>
-__device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &sm, unsigned unit,
+template <typename OffT, class F, bool STATS, int PHASE, class SMT>
+__device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &sm, unsigned unit,
                                          int p, unsigned long long &my_conf,
                                          unsigned long long *my_edges) {
     const RoundCfg &rc = sm.rc;
     const int np = p ^ 1;
+    if constexpr (F::small) {  // only bin-0 units exist
+        bin0_chunk<OffT, F, STATS, PHASE>(P, ro, sm, unit - rc.ubase[4], np, my_conf, my_edges);
+        return;
+    } else {
     const unsigned *ub = rc.ubase;
     const bool is_hub = unit < ub[1];
     if (is_hub && rc.hub_split) {
@@ -974,54 +1053,13 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, Smem &
     } else if (unit < ub[4]) {
         group_chunk<8, OffT, F, STATS, PHASE>(P, ro, sm, 1, unit - ub[3], np, my_conf, my_edges);
     } else {
-        // ---- bin 0 chunk
-        const unsigned c = unit - ub[4];
-        const unsigned csz0 = rc.csz[0];
-        const unsigned long long lo = (unsigned long long)c * csz0;
-        const unsigned long long hi = min(lo + csz0, rc.L[0].total);
-        int *out = dyn_list(P, np, 0) + (long long)c * csz0;
-        // order-preserving compaction of the losers (index order j-major, then
-        // thread), ONE barrier per tile: every warp publishes its per-j loser
-        // counts into a double-buffered table and scans it itself.  (Order only
-        // affects locality, but an unordered list fragments round after round.)
-        const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-        unsigned written = 0, buf = 0;
-        for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NPT) {
-            int u[NPT];
-            bool lost[NPT];
-            small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
-            if (PHASE == 1) {
-                unsigned bal[NPT];
-#pragma unroll
-                for (int j = 0; j < NPT; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
-                if (lane < NPT) {
-                    unsigned mine = 0;
-#pragma unroll
-                    for (int j = 0; j < NPT; ++j)
-                        if (lane == (unsigned)j) mine = __popc(bal[j]);
-                    sm.cnt_tab[buf][lane * NW + warp] = mine;
-                }
-                __syncthreads();
-                unsigned run = written;
-#pragma unroll
-                for (int j = 0; j < NPT; ++j) {
-                    const unsigned v = lane < NW ? sm.cnt_tab[buf][j * NW + lane] : 0u;
-                    const unsigned incl = warp_incl_scan(v);
-                    const unsigned before = __shfl_sync(FULL, incl - v, warp);  // warps < me in slice j
-                    const unsigned tot_j = __shfl_sync(FULL, incl, 31);
-                    if (lost[j]) out[run + before + __popc(bal[j] & lanemask_lt())] = u[j];
-                    run += tot_j;
-                }
-                written = run;
-                buf ^= 1u;
-            }
-        }
-        if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 0, c, written);
+        bin0_chunk<OffT, F, STATS, PHASE>(P, ro, sm, unit - ub[4], np, my_conf, my_edges);
+    }
     }
 }
 
-template <typename OffT, class F, bool STATS, int PHASE>
-__device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem &sm, int p,
+template <typename OffT, class F, bool STATS, int PHASE, class SMT>
+__device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, SMT &sm, int p,
                                           unsigned long long &my_conf, unsigned long long *my_edges) {
     unsigned *ctr = &P.ctrl->unit_ctr[PHASE][p];
     if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);
@@ -1039,8 +1077,9 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, Smem 
 
 // ------------------------------------------------------------------ kernel
 template <typename OffT, class F, bool STATS>
-__global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
-    __shared__ Smem sm;
+__global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) solve_kernel(Params P) {
+    constexpr int NSB = F::small ? 1 : NSEG_BINS;  // segmented bins present
+    __shared__ SmemT<F::small> sm;
     Ctrl *C = P.ctrl;
     const OffT *ro = reinterpret_cast<const OffT *>(P.ro);
     const unsigned lane = lane_id();
@@ -1087,7 +1126,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         //      previous round's output (round 1: the full static lists)
         if (t > 1) {
 #pragma unroll 1
-            for (int b = 0; b < NSEG_BINS; ++b) {
+            for (int b = 0; b < NSB; ++b) {
                 const unsigned ns = rc.prev_nseg[b];
                 if (ns == 0) {  // CTA-uniform
                     if (threadIdx.x == 0) sm.prefix[b][0] = 0;
@@ -1126,10 +1165,15 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
             }
         }
         if (threadIdx.x == 0) {
-            for (int b = 0; b < NSEG_BINS; ++b)
+            for (int b = 0; b < NSEG_BINS; ++b) {
+                if (F::small && b > 0) {  // empty bins (SmemT<true> keeps one prefix)
+                    rc.L[b] = List{rc.stat_lists[b], 0, 0, 0, false};
+                    continue;
+                }
                 rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.nst[b], 0, 0, false}
-                                 : List{dyn_list(P, p, b), sm.prefix[b][rc.prev_nseg[b]], rc.prev_nseg[b],
-                                        rc.prev_cap[b], true};
+                                 : List{dyn_list(P, p, b), sm.prefix[F::small ? 0 : b][rc.prev_nseg[b]],
+                                        rc.prev_nseg[b], rc.prev_cap[b], true};
+            }
             const unsigned long long hub_total = t == 1 ? rc.nst[BIN_HUB] : ld_relaxed_u64(&C->hub_cnt[p]);
             rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : dyn_list(P, p, BIN_HUB), hub_total, 0, 0, false};
             unsigned long long s = 0;  // this rank's |W_t| (the whole |W_t| on one GPU)
@@ -1143,7 +1187,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
                 for (int b = 0; b < NBIN; ++b) rc.L[b] = List{rc.stat_lists[b], rc.nst[b], 0, 0, false};
             rc.topo = topo;
             rc.ident = topo && rc.ident_small;
-            rc.csz[0] = chunk_size(rc.L[0].total, BLOCK * NPT);
+            rc.csz[0] = chunk_size(rc.L[0].total, BLOCK * (F::small ? NPT_SMALL : NPT));
             rc.csz[1] = chunk_size(rc.L[1].total, NW * 4);
             rc.csz[2] = chunk_size(rc.L[2].total, NW * 2);
             rc.csz[3] = (bin3_cta && rc.L[3].total <= MAXSEG) ? 1u : chunk_size(rc.L[3].total, NW);
@@ -1191,7 +1235,7 @@ __global__ void __launch_bounds__(BLOCK, MIN_CTAS) solve_kernel(Params P) {
         __syncthreads();
         if (s == 0) break;  // worklist drained (driver.py:145)
         if (F::mg && blockIdx.x == 0 && threadIdx.x == 0) C->rounds = t;  // progress (timeout report)
-        if (rc.hub_split) {  // CTA-uniform: equal-size edge slices over the active hubs
+        if (!F::small && rc.hub_split) {  // CTA-uniform: equal-size edge slices over the active hubs
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
             unsigned long long e_loc = 0;
             for (unsigned i = threadIdx.x; i < H; i += BLOCK) {
@@ -1380,22 +1424,30 @@ static const void *kernel_ptr() {
     return (const void *)solve_kernel<OffT, F, STATS>;
 }
 
-// the instantiation for (offset width, state width, column format, stats)
-static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats) {
-    if (!narrow) return stats ? kernel_ptr<long long, F32, true>() : kernel_ptr<long long, F32, false>();
-    if (x16 && c16) return stats ? kernel_ptr<int, F16D, true>() : kernel_ptr<int, F16D, false>();
-    if (x16) return stats ? kernel_ptr<int, F16, true>() : kernel_ptr<int, F16, false>();
-    if (c16) return stats ? kernel_ptr<int, F32D, true>() : kernel_ptr<int, F32D, false>();
-    return stats ? kernel_ptr<int, F32, true>() : kernel_ptr<int, F32, false>();
+template <class F32_, class F16_, class F16D_, class F32D_, bool STATS>
+static const void *pick(bool narrow, bool x16, bool c16) {
+    if (!narrow) return x16 ? kernel_ptr<long long, F16_, STATS>() : kernel_ptr<long long, F32_, STATS>();
+    if (x16 && c16) return kernel_ptr<int, F16D_, STATS>();
+    if (x16) return kernel_ptr<int, F16_, STATS>();
+    if (c16) return kernel_ptr<int, F32D_, STATS>();
+    return kernel_ptr<int, F32_, STATS>();
+}
+
+// the instantiation for (offset width, state width, column format, bin-0
+// only, stats).  int64 offsets (m >= 2^31) keep 32-bit words.
+static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats, bool small = false) {
+    if (!narrow) x16 = c16 = false;
+    if (small)
+        return stats ? pick<SF32, SF16, SF16D, SF32D, true>(narrow, x16, c16)
+                     : pick<SF32, SF16, SF16D, SF32D, false>(narrow, x16, c16);
+    return stats ? pick<F32, F16, F16D, F32D, true>(narrow, x16, c16)
+                 : pick<F32, F16, F16D, F32D, false>(narrow, x16, c16);
 }
 
 // multi-GPU instantiations (no per-round edge statistics)
-static const void *select_kernel_mg(bool narrow, bool x16, bool c16) {
-    if (!narrow) return x16 ? kernel_ptr<long long, MF16, false>() : kernel_ptr<long long, MF32, false>();
-    if (x16 && c16) return kernel_ptr<int, MF16D, false>();
-    if (x16) return kernel_ptr<int, MF16, false>();
-    if (c16) return kernel_ptr<int, MF32D, false>();
-    return kernel_ptr<int, MF32, false>();
+static const void *select_kernel_mg(bool narrow, bool x16, bool c16, bool small = false) {
+    if (small) return pick<SMF32, SMF16, SMF16D, SMF32D, false>(narrow, x16, c16);
+    return pick<MF32, MF16, MF16D, MF32D, false>(narrow, x16, c16);
 }
 
 static int occupancy_of(const void *fn) {
@@ -1414,7 +1466,7 @@ static int occupancy() {
 
 // format overrides (tests / experiments): force int64 offsets, forbid the
 // 16-bit state word, forbid 16-bit delta columns
-static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0;
+static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0;
 
 // Per-solve preprocessing shared by hc_solve and hc_mg_solve, for the owned
 // range [lo, lo + nown): fresh control block, static degree-bucketed lists,
@@ -1519,6 +1571,11 @@ int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16) {
     return HC_OK;
 }
 
+int hc_solve_set_small(int allow) {
+    g_no_small = allow ? 0 : 1;
+    return HC_OK;
+}
+
 int hc_device_info(int *h_num_sms, int *h_ctas_per_sm) {
     if (h_num_sms) *h_num_sms = num_sms();
     if (h_ctas_per_sm) *h_ctas_per_sm = occupancy();
@@ -1581,9 +1638,9 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     const bool x16_exact = pr.tot[9] + pr.tot[10] + pr.tot[11] + pr.tot[12] == 0;
     bool x16 = (HC_FMT16 != 0) && !g_no_x16;
     const bool c16 = pr.c16_ok;
-    const int per_sm = occupancy();
-    HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
-    P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
+    // bin-0-only graphs (every degree <= 16) run the SMALL kernel
+    bool small = !g_no_small;
+    for (int k = 1; k < NKEY; ++k) small = small && pr.tot[k] == 0;
     long long info[3];
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) {  // fresh control block (keeps nstat via copy_totals)
@@ -1595,7 +1652,10 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
                 HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
         }
         void *args[] = {&P};
-        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr);
+        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr, small);
+        const int per_sm = occupancy_of(fn);
+        HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
+        P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
         HC_CUDA_TRY(cudaLaunchCooperativeKernel(fn, dim3(P.nblocks), dim3(BLOCK), args, 0, st));
         HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
         HC_CUDA_TRY(cudaStreamSynchronize(st));
@@ -1710,7 +1770,9 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
     P.mbox = reinterpret_cast<Mbox *>(tab[MG_MAX_WORLD + rank]);
     // every rank must pick the same state-word width: decided on the whole graph
     const bool x16 = (HC_FMT16 != 0) && !g_no_x16 && pr.max_degree <= 16384ull;
-    const void *fn = select_kernel_mg(pr.narrow, x16, pr.c16_ok);
+    bool small = !g_no_small;
+    for (int k = 1; k < NKEY; ++k) small = small && pr.tot[k] == 0;
+    const void *fn = select_kernel_mg(pr.narrow, x16, pr.c16_ok, small);
     const int per_sm = occupancy_of(fn);
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_mg_solve: occupancy query failed");
     const unsigned full = (unsigned)(per_sm * std::max(1, num_sms()));

@@ -256,18 +256,22 @@ def test_storage_formats_vs_oracle(leaves, extra):
 
 @pytest.mark.parametrize("fmt", [(1, 1, 1), (0, 1, 1), (0, 0, 1), (0, 1, 0)])
 def test_forced_storage_formats_vs_golden(configs, fmt):
-    """Every (offset width, state width, column format) instantiation on the
-    reference-recorded C1 graph (RMAT-16) and a grid."""
+    """Every (offset width, state width, column format) instantiation, with
+    and without the bin-0-only kernel, on the reference-recorded C1 graph
+    (RMAT-16) and a grid (bin-0 only)."""
     L = hc._lib.load()
     L.hc_solve_set_formats(*fmt)
     try:
-        for key in ("rmat16", "grid64x96"):
-            kind, kw = CONFIG_SPECS[key]
-            want = configs[key]
-            dg = _device_graph(kind, kw)
-            for mode in MODES:
-                colors, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
-                assert np.array_equal(colors, want["colors"]), (key, mode, fmt)
-                assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt)
+        for small in (1, 0):
+            L.hc_solve_set_small(small)
+            for key in ("rmat16", "grid64x96"):
+                kind, kw = CONFIG_SPECS[key]
+                want = configs[key]
+                dg = _device_graph(kind, kw)
+                for mode in MODES:
+                    colors, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+                    assert np.array_equal(colors, want["colors"]), (key, mode, fmt, small)
+                    assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt, small)
     finally:
         L.hc_solve_set_formats(0, 0, 0)
+        L.hc_solve_set_small(1)
