@@ -668,41 +668,54 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
 }
 
 // ------------------------------------------------------------------ bin 0
-// Thread per node, NP nodes per thread (NPT, or NPT_SMALL in the bin-0-only kernel); all list / offset / first-four-
-// neighbour loads of the NP nodes are issued before any is consumed.
-template <typename OffT, class F, bool STATS, int PHASE>
-__device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, const RoundCfg &rc,
+// Thread per node, NP nodes per thread (NPT, or NPT_SMALL in the bin-0-only
+// kernel).  A tile is issued (list entry, row offsets, activity / tentative
+// word of its NP nodes: tile_issue) and then finished (first-four-neighbour
+// column loads, X gathers, mex / conflict count, writes: tile_finish); all
+// loads of one stage are issued before any is consumed.  (Issuing tile i+1
+// before finishing tile i was measured slower: grid4096 609 -> 752+ ms.)
+template <typename OffT, int NP>
+struct TileA {
+    int u[NP];
+    OffT rb[NP], re[NP];
+    unsigned xu[NP];
+};
+
+template <typename OffT, class F, int NP, int PHASE>
+__device__ __forceinline__ void tile_issue(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
-                                           unsigned long long hi, int *u, bool *lost,
-                                           unsigned long long &my_conf, unsigned long long *my_edges) {
-    constexpr int NP = F::small ? NPT_SMALL : NPT;
+                                           unsigned long long hi, TileA<OffT, NP> &a) {
     const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
-    unsigned xu[NP];
     unsigned seg = ident ? 0u : list_segment(L, prefix, base);  // same for the whole CTA (broadcast)
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
         const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
-        u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
-        lost[j] = false;
-        xu[j] = 0u;
+        a.u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
     }
     // the row offsets are loaded together with the activity word (speculative
     // for inactive nodes in topology sweeps): one dependent round trip less
-    OffT rb[NP], re[NP];
 #pragma unroll
     for (int j = 0; j < NP; ++j) {
-        rb[j] = u[j] >= 0 ? ro[u[j]] : OffT(0);
-        re[j] = u[j] >= 0 ? ro[u[j] + 1] : OffT(0);
+        a.rb[j] = a.u[j] >= 0 ? ro[a.u[j]] : OffT(0);
+        a.re[j] = a.u[j] >= 0 ? ro[a.u[j] + 1] : OffT(0);
     }
-    if (topo || PHASE == 1) {
 #pragma unroll
-        for (int j = 0; j < NP; ++j) xu[j] = u[j] >= 0 ? xget<F>(P, u[j]) : 0u;
-        if (topo) {
+    for (int j = 0; j < NP; ++j) a.xu[j] = ((topo || PHASE == 1) && a.u[j] >= 0) ? xget<F>(P, a.u[j]) : 0u;
+}
+
+template <typename OffT, class F, bool STATS, int PHASE, int NP>
+__device__ __forceinline__ void tile_finish(const Params &P, const RoundCfg &rc, TileA<OffT, NP> &a, bool *lost,
+                                            unsigned long long &my_conf, unsigned long long *my_edges) {
+    int *u = a.u;
+    OffT *rb = a.rb, *re = a.re;
+    const unsigned *xu = a.xu;
 #pragma unroll
-            for (int j = 0; j < NP; ++j)
-                if (xu[j] & FB<F>) { u[j] = -1; re[j] = rb[j]; }  // inactive (_kernels.pyx:76-77, 135-136)
-        }
+    for (int j = 0; j < NP; ++j) lost[j] = false;
+    if (rc.topo) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j)
+            if (xu[j] & FB<F>) { u[j] = -1; re[j] = rb[j]; }  // inactive (_kernels.pyx:76-77, 135-136)
     }
     int nb[NP][4];
 #pragma unroll
@@ -921,6 +934,16 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
     return total;
 }
 
+template <typename OffT, class F, bool STATS, int PHASE>
+__device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, const RoundCfg &rc,
+                                           const unsigned *prefix, unsigned long long base,
+                                           unsigned long long hi, TileA<OffT, F::small ? NPT_SMALL : NPT> &a,
+                                           bool *lost, unsigned long long &my_conf, unsigned long long *my_edges) {
+    constexpr int NP = F::small ? NPT_SMALL : NPT;
+    tile_issue<OffT, F, NP, PHASE>(P, ro, rc, prefix, base, hi, a);
+    tile_finish<OffT, F, STATS, PHASE, NP>(P, rc, a, lost, my_conf, my_edges);
+}
+
 // A chunk of bin 0 (thread per node, NP nodes per thread per tile).
 template <typename OffT, class F, bool STATS, int PHASE, class SMT>
 __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT &sm, unsigned c, int np,
@@ -938,9 +961,10 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     unsigned written = 0, buf = 0;
     for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NP) {
-        int u[NP];
+        TileA<OffT, NP> cur;
         bool lost[NP];
-        small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, u, lost, my_conf, my_edges);
+        small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, cur, lost, my_conf, my_edges);
+        const int *u = cur.u;
         if (PHASE == 1) {
             unsigned bal[NP];
 #pragma unroll
@@ -1770,8 +1794,10 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
     P.mbox = reinterpret_cast<Mbox *>(tab[MG_MAX_WORLD + rank]);
     // every rank must pick the same state-word width: decided on the whole graph
     const bool x16 = (HC_FMT16 != 0) && !g_no_x16 && pr.max_degree <= 16384ull;
-    bool small = !g_no_small;
-    for (int k = 1; k < NKEY; ++k) small = small && pr.tot[k] == 0;
+    // the kernel family is a whole-graph decision too: ranks sharing one GPU
+    // (tests) must run kernels with the same shared-memory footprint to
+    // co-reside (an SM's carve-out cannot change while a CTA lives on it)
+    const bool small = !g_no_small && pr.max_degree <= 16ull;
     const void *fn = select_kernel_mg(pr.narrow, x16, pr.c16_ok, small);
     const int per_sm = occupancy_of(fn);
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_mg_solve: occupancy query failed");
