@@ -95,6 +95,10 @@ constexpr int NSEG_BINS = 4;             // bins 0..3 are segmented; bin 4 (hubs
 constexpr int BIN_HUB = 4;
 constexpr int NBIN = 5;
 constexpr int HUB_MIN = 4097;            // deg >= HUB_MIN -> hub
+#ifndef HC_HUB_U
+#define HC_HUB_U 8
+#endif
+constexpr int HU = HC_HUB_U;             // column loads in flight per thread in the CTA-per-node paths
 constexpr int HUB_WORDS = 512;           // CTA bitmap window: 16384 colors per pass
 constexpr int WIN_WORDS = 32;            // warp bitmap window: 1024 colors per pass
 constexpr int MAXSEG = 2048;             // output segments per bin per round
@@ -166,6 +170,10 @@ struct Params {
     void *X;                   // state words (Fmt XT)
     int *stat;                 // static lists, bins contiguous
     int *dyn[2][NBIN];         // dynamic lists per parity and bin
+    // (row offset << 16 | degree) of every list entry of bins 0-3, so a list
+    // read yields the adjacency range without a dependent row-offset load
+    unsigned long long *stat_od;
+    unsigned long long *dyn_od[2][NSEG_BINS];
     Ctrl *ctrl;
     hc_round_rec *rec;
     long long max_rec;
@@ -190,6 +198,7 @@ struct Params {
 // previous round's output: nseg segments of capacity segcap).
 struct List {
     const int *base;
+    const unsigned long long *od;  // per entry: row offset << 16 | degree (bins 0-3)
     unsigned long long total;
     unsigned nseg, segcap;
     bool segmented;
@@ -200,6 +209,7 @@ struct List {
 struct RoundCfg {
     List L[NBIN];
     const int *stat_lists[NBIN];
+    const unsigned long long *stat_od[NBIN];
     unsigned long long nst[NBIN];
     unsigned csz[NSEG_BINS], nch[NSEG_BINS];
     unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
@@ -234,6 +244,15 @@ using Smem = SmemT<false>;
 __device__ __forceinline__ int *dyn_list(const Params &P, int p, int b) {
     return p ? P.dyn[1][b] : P.dyn[0][b];
 }
+__device__ __forceinline__ unsigned long long *dyn_od(const Params &P, int p, int b) {
+    return p ? P.dyn_od[1][b] : P.dyn_od[0][b];
+}
+__device__ __forceinline__ unsigned long long make_od(long long b, long long e) {
+    return ((unsigned long long)b << 16) | (unsigned long long)(e - b);
+}
+// list entry loads (plain loads: __ldcg here cost the grid 5%, 608 -> 640 ms)
+__device__ __forceinline__ int ld_entry(const int *p) { return *p; }
+__device__ __forceinline__ unsigned long long ld_od(const unsigned long long *p) { return *p; }
 
 __device__ __forceinline__ long long list_index(const List &L, const unsigned *prefix, unsigned long long v) {
     if (!L.segmented) return (long long)v;
@@ -498,18 +517,22 @@ template <int G, typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, const List &L,
                                            const unsigned *prefix, unsigned long long v0,
                                            unsigned long long hi, bool topo, int *out,
-                                           unsigned *out_cnt, unsigned *bm,
+                                           unsigned long long *out_od, unsigned *out_cnt, unsigned *bm,
                                            unsigned long long &my_conf, unsigned long long *my_edges) {
     const unsigned lane = lane_id();
     const unsigned sub = lane % G, gi = lane / G;
     const unsigned long long v = v0 + gi;
-    int u = v < hi ? L.base[list_index(L, prefix, v)] : -1;
+    // the list entry carries the adjacency range (no dependent row-offset load)
+    const long long idx = v < hi ? list_index(L, prefix, v) : -1;
+    int u = idx >= 0 ? ld_entry(L.base + idx) : -1;
+    const unsigned long long od = idx >= 0 ? ld_od(L.od + idx) : 0ull;
     unsigned xu = 0;
     if (topo || PHASE == 1) {
         xu = u >= 0 ? xget<F>(P, u) : 0u;
         if (topo && (xu & FB<F>)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
     }
-    const long long b = u >= 0 ? (long long)ro[u] : 0, e = u >= 0 ? (long long)ro[u + 1] : 0;
+    const long long b = u >= 0 ? (long long)(od >> 16) : 0;
+    const long long e = u >= 0 ? b + (long long)(od & 0xffffull) : 0;
     unsigned iters = (unsigned)((e - b + 4 * G - 1) / (4 * G));
     iters = __reduce_max_sync(FULL, iters);
     unsigned long long mask = 0;
@@ -587,8 +610,13 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
         if (sub == 0 && u >= 0) {
             my_conf += cnt;
             if (STATS) my_edges[1] += low;
-            if (cnt) out[atomicAdd(out_cnt, 1u)] = u;
-            else xput<F>(P, u, xu | FB<F>);
+            if (cnt) {
+                const unsigned pos = atomicAdd(out_cnt, 1u);
+                out[pos] = u;
+                out_od[pos] = od;
+            } else {
+                xput<F>(P, u, xu | FB<F>);
+            }
         }
     }
 }
@@ -603,15 +631,15 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
         if (threadIdx.x == 0) sm.hub_first = 0x7fffffff;
         __syncthreads();
         const unsigned hi = min(lim, w0 + HUB_WORDS * 32);
-        for (long long k = b + threadIdx.x; k < e; k += 4 * BLOCK) {
-            int v[4];
+        for (long long k = b + threadIdx.x; k < e; k += HU * BLOCK) {
+            int v[HU];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = (k + q * BLOCK < e) ? colget<F, true>(P, k + q * BLOCK, u) : -1;
-            unsigned x[4];
+            for (int q = 0; q < HU; ++q) v[q] = (k + q * BLOCK < e) ? colget<F, true>(P, k + q * BLOCK, u) : -1;
+            unsigned x[HU];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
+            for (int q = 0; q < HU; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < HU; ++q) {
                 const unsigned c = x[q] & CM<F>;
                 if ((x[q] & FB<F>) && c > w0 && c <= hi) mark(sm.hub_bm, c - w0);
             }
@@ -638,19 +666,19 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
     if (threadIdx.x == 0) sm.red = 0;
     __syncthreads();
     unsigned cnt = 0, low = 0;
-    for (long long k0 = b + (long long)warp * 128; k0 < e; k0 += 128LL * NW) {
-        int v[4];
+    for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
+        int v[HU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < HU; ++q) {
             const long long k = k0 + 32 * q + lane;
             v[q] = k < e ? colget<F, true>(P, k, u) : 0x7fffffff;
         }
-        unsigned x[4];
+        unsigned x[HU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
+        for (int q = 0; q < HU; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
         bool stop = false;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < HU; ++q) {
             if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
             else stop = true;
         }
@@ -688,17 +716,33 @@ __device__ __forceinline__ void tile_issue(const Params &P, const OffT *ro, cons
     const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
     unsigned seg = ident ? 0u : list_segment(L, prefix, base);  // same for the whole CTA (broadcast)
+    // bin-0-only graphs (grids, meshes) read the row offsets: their lists are
+    // nearly id-ordered, so the offsets are almost contiguous, and a 4-byte
+    // list entry beats the 12-byte (id, od) pair (grid4096 data 843 vs 969 ms)
+    if (ident || F::small) {
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-        const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
-        a.u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : L.base[list_index_walk(L, prefix, v, seg)]) : -1;
-    }
-    // the row offsets are loaded together with the activity word (speculative
-    // for inactive nodes in topology sweeps): one dependent round trip less
+        for (int j = 0; j < NP; ++j) {
+            const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
+            a.u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : ld_entry(L.base + list_index_walk(L, prefix, v, seg)))
+                            : -1;
+        }
+        // the row offsets are loaded together with the activity word
+        // (speculative for inactive nodes): one dependent round trip less
 #pragma unroll
-    for (int j = 0; j < NP; ++j) {
-        a.rb[j] = a.u[j] >= 0 ? ro[a.u[j]] : OffT(0);
-        a.re[j] = a.u[j] >= 0 ? ro[a.u[j] + 1] : OffT(0);
+        for (int j = 0; j < NP; ++j) {
+            a.rb[j] = a.u[j] >= 0 ? ro[a.u[j]] : OffT(0);
+            a.re[j] = a.u[j] >= 0 ? ro[a.u[j] + 1] : OffT(0);
+        }
+    } else {  // list entries carry (row offset, degree)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
+            const long long idx = v < hi ? list_index_walk(L, prefix, v, seg) : -1;
+            a.u[j] = idx >= 0 ? ld_entry(L.base + idx) : -1;
+            const unsigned long long od = idx >= 0 ? ld_od(L.od + idx) : 0ull;
+            a.rb[j] = (OffT)(od >> 16);
+            a.re[j] = a.rb[j] + (OffT)(od & 0xffffull);
+        }
     }
 #pragma unroll
     for (int j = 0; j < NP; ++j) a.xu[j] = ((topo || PHASE == 1) && a.u[j] >= 0) ? xget<F>(P, a.u[j]) : 0u;
@@ -796,11 +840,12 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
     const unsigned long long lo = (unsigned long long)c * csz;
     const unsigned long long hi = min(lo + csz, rc.L[bin].total);
     int *out = dyn_list(P, np, bin) + (long long)c * csz;
+    unsigned long long *out_od = dyn_od(P, np, bin) + (long long)c * csz;
     if (threadIdx.x == 0) sm.out_cnt = 0;
     __syncthreads();
     constexpr unsigned NG = 32 / G;
     for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG)
-        group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out,
+        group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out, out_od,
                                           &sm.out_cnt, sm.win_bm[warp], my_conf, my_edges);
     __syncthreads();
     if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, c, sm.out_cnt);
@@ -818,15 +863,15 @@ __device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigne
     for (int i = threadIdx.x; i < HA_WORDS + 2; i += BLOCK) sm.hub_bm[i] = 0u;  // [0,1]: mask, [2..]: words
     __syncthreads();
     unsigned long long mask = 0;
-    for (long long kk = b + threadIdx.x; kk < e; kk += 4 * BLOCK) {
-        int v[4];
+    for (long long kk = b + threadIdx.x; kk < e; kk += HU * BLOCK) {
+        int v[HU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = (kk + q * BLOCK < e) ? colget<F, true>(P, kk + q * BLOCK, u) : -1;
-        unsigned x[4];
+        for (int q = 0; q < HU; ++q) v[q] = (kk + q * BLOCK < e) ? colget<F, true>(P, kk + q * BLOCK, u) : -1;
+        unsigned x[HU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
+        for (int q = 0; q < HU; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < HU; ++q) {
             const unsigned c = x[q] & CM<F>;
             if (!(x[q] & FB<F>)) continue;
             if (c <= 64u) mask |= 1ull << (c - 1u);
@@ -887,19 +932,19 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
     const long long b = b0 + len * slice / k, e = b0 + len * (slice + 1) / k;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     unsigned cnt = 0, low = 0;
-    for (long long k0 = b + (long long)warp * 128; k0 < e; k0 += 128LL * NW) {
-        int v[4];
+    for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
+        int v[HU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < HU; ++q) {
             const long long kk = k0 + 32 * q + lane;
             v[q] = kk < e ? colget<F, true>(P, kk, u) : 0x7fffffff;
         }
-        unsigned x[4];
+        unsigned x[HU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
+        for (int q = 0; q < HU; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
         bool stop = false;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < HU; ++q) {
             if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
             else stop = true;
         }
@@ -954,6 +999,7 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     const unsigned long long lo = (unsigned long long)c * csz0;
     const unsigned long long hi = min(lo + csz0, rc.L[0].total);
     int *out = dyn_list(P, np, 0) + (long long)c * csz0;
+    unsigned long long *out_od = dyn_od(P, np, 0) + (long long)c * csz0;
     // order-preserving compaction of the losers (index order j-major, then
     // thread), ONE barrier per tile: every warp publishes its per-j loser
     // counts into a double-buffered table and scans it itself.  (Order only
@@ -984,7 +1030,11 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
                 const unsigned incl = warp_incl_scan(v);
                 const unsigned before = __shfl_sync(FULL, incl - v, warp);  // warps < me in slice j
                 const unsigned tot_j = __shfl_sync(FULL, incl, 31);
-                if (lost[j]) out[run + before + __popc(bal[j] & lanemask_lt())] = u[j];
+                if (lost[j]) {
+                    const unsigned pos = run + before + __popc(bal[j] & lanemask_lt());
+                    out[pos] = u[j];
+                    if constexpr (!F::small) out_od[pos] = make_od(cur.rb[j], cur.re[j]);
+                }
                 run += tot_j;
             }
             written = run;
@@ -1061,7 +1111,10 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                     if (STATS) my_edges[1] += low;
                     if (k) {
                         if (is_hub) dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
-                        else dyn_list(P, np, 3)[c] = u;  // segment c, capacity 1
+                        else {  // segment c, capacity 1
+                            dyn_list(P, np, 3)[c] = u;
+                            dyn_od(P, np, 3)[c] = make_od(ro[u], ro[u + 1]);
+                        }
                         pushed = 1;
                     } else {
                         xput<F>(P, u, xu | FB<F>);
@@ -1118,6 +1171,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         for (int b = 0; b < NBIN; ++b) {
             rc.nst[b] = C->nstat[b];
             rc.stat_lists[b] = P.stat + off;
+            rc.stat_od[b] = P.stat_od + off;
             off += rc.nst[b];
         }
         rc.ident_small = rc.nst[0] == (unsigned long long)P.nown;  // all nodes in bin 0: sweep ids
@@ -1191,15 +1245,16 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         if (threadIdx.x == 0) {
             for (int b = 0; b < NSEG_BINS; ++b) {
                 if (F::small && b > 0) {  // empty bins (SmemT<true> keeps one prefix)
-                    rc.L[b] = List{rc.stat_lists[b], 0, 0, 0, false};
+                    rc.L[b] = List{rc.stat_lists[b], rc.stat_od[b], 0, 0, 0, false};
                     continue;
                 }
-                rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.nst[b], 0, 0, false}
-                                 : List{dyn_list(P, p, b), sm.prefix[F::small ? 0 : b][rc.prev_nseg[b]],
+                rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false}
+                                 : List{dyn_list(P, p, b), dyn_od(P, p, b), sm.prefix[F::small ? 0 : b][rc.prev_nseg[b]],
                                         rc.prev_nseg[b], rc.prev_cap[b], true};
             }
             const unsigned long long hub_total = t == 1 ? rc.nst[BIN_HUB] : ld_relaxed_u64(&C->hub_cnt[p]);
-            rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : dyn_list(P, p, BIN_HUB), hub_total, 0, 0, false};
+            rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : dyn_list(P, p, BIN_HUB), nullptr, hub_total, 0, 0,
+                                 false};
             unsigned long long s = 0;  // this rank's |W_t| (the whole |W_t| on one GPU)
             for (int b = 0; b < NBIN; ++b) s += rc.L[b].total;
             // global |W_t|: multi-GPU sums over ranks at the end-of-round barrier
@@ -1208,7 +1263,8 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             // bin-3 nodes at CTA granularity when few are active (latency regime)
             const bool bin3_cta = rc.L[3].total <= 2ull * P.nblocks;
             if (topo)  // topology-driven: sweep the static lists, activity test
-                for (int b = 0; b < NBIN; ++b) rc.L[b] = List{rc.stat_lists[b], rc.nst[b], 0, 0, false};
+                for (int b = 0; b < NBIN; ++b)
+                    rc.L[b] = List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false};
             rc.topo = topo;
             rc.ident = topo && rc.ident_small;
             rc.csz[0] = chunk_size(rc.L[0].total, BLOCK * (F::small ? NPT_SMALL : NPT));
@@ -1396,6 +1452,17 @@ __global__ void delta_columns_kernel(const long long *ro, const int *ci, long lo
     }
 }
 
+// (row offset << 16 | degree) of every static list entry (degrees above
+// 0xffff -- hubs only, which never read it -- are clamped)
+__global__ void fill_od_kernel(const long long *ro, const int *stat, long long count, unsigned long long *od) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (long long)gridDim.x * blockDim.x) {
+        const int u = stat[i];
+        const long long b = ro[u], d = ro[u + 1] - b;
+        od[i] = ((unsigned long long)b << 16) | (unsigned long long)(d < 0xffff ? d : 0xffff);
+    }
+}
+
 // max degree over all nodes (the multi-GPU state-word format must agree on
 // every rank, so it is decided from the whole graph)
 __global__ void max_degree_kernel(const long long *ro, long long n, unsigned long long *out) {
@@ -1413,7 +1480,8 @@ inline size_t seg_capacity(long long cnt) {
 }
 
 struct Layout {
-    size_t ctrl, x, stat, dyn[2][NBIN], ro32, ci16, hub_acc, part, bnd, ptrs, maxdeg, total;
+    size_t ctrl, x, stat, dyn[2][NBIN], stat_od, dyn_od[2][NSEG_BINS], ro32, ci16, hub_acc, part, bnd, ptrs,
+        maxdeg, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
@@ -1431,6 +1499,12 @@ static Layout layout(long long n, long long m, long long nown, bool mg) {
         for (int b = 0; b < NBIN; ++b) {
             L.dyn[p][b] = o;
             o = align_up(o + 4 * (b == BIN_HUB ? (size_t)nown : seg_capacity(nown)), 256);
+        }
+    L.stat_od = o; o = align_up(o + 8 * (size_t)nown, 256);
+    for (int p = 0; p < 2; ++p)
+        for (int b = 0; b < NSEG_BINS; ++b) {
+            L.dyn_od[p][b] = o;
+            o = align_up(o + 8 * seg_capacity(nown), 256);
         }
     L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
     L.ci16 = o; o = align_up(o + (m < 0x7fffffffLL ? 2 * (size_t)m : 0) + 256, 256);
@@ -1514,6 +1588,9 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     P.stat = reinterpret_cast<int *>(ws + L.stat);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) P.dyn[p][b] = reinterpret_cast<int *>(ws + L.dyn[p][b]);
+    P.stat_od = reinterpret_cast<unsigned long long *>(ws + L.stat_od);
+    for (int p = 0; p < 2; ++p)
+        for (int b = 0; b < NSEG_BINS; ++b) P.dyn_od[p][b] = reinterpret_cast<unsigned long long *>(ws + L.dyn_od[p][b]);
     P.fmt_overflow = &P.ctrl->fmt_overflow;
     const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
     P.ro = narrow ? (const void *)(ws + L.ro32) : (const void *)d_row_offsets;
@@ -1524,6 +1601,10 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     const int sms = std::max(1, num_sms());
     copy_totals_kernel<<<1, 32, 0, st>>>(out.d_totals, P.ctrl);
     HC_CHECK_LAUNCH();
+    if (P.nown > 0) {
+        fill_od_kernel<<<sms * 8, 256, 0, st>>>(ro64, P.stat, P.nown, P.stat_od);
+        HC_CHECK_LAUNCH();
+    }
     if (narrow) {
         narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro64, reinterpret_cast<int *>(ws + L.ro32), n + 1);
         HC_CHECK_LAUNCH();
