@@ -4,7 +4,7 @@
 // (pkg/src/hybridcolor/driver.py:122-176) together with the round functions
 // (coloring.py:113-176), the kernels (_kernels.pyx:29-149) and the worklist
 // swap (worklist.py:77-91) by ONE cooperatively launched persistent kernel
-// (two 512-thread CTAs per SM): every round is
+// (three 512-thread CTAs per SM): every round is
 //     assign -> grid barrier -> resolve -> grid barrier
 // with the hybrid mode decision, the worklist and the per-round records kept
 // on the device, so there is no host round trip per round.
@@ -31,7 +31,7 @@
 //
 // Work distribution (IrGL-style nested parallelism).
 // Nodes are binned once by degree; each bin has its own granularity:
-//   bin 0  deg <= 16        one thread per node, NPT=4 nodes per thread with
+//   bin 0  deg <= 16        one thread per node, NPT=2 nodes per thread with
 //                           all their loads batched (memory-level parallelism)
 //   bin 1  17..32           a group of 8 lanes per node (4 nodes per warp)
 //   bin 2  33..64           16 lanes per node (2 per warp)
@@ -70,14 +70,14 @@ namespace solve {
 #define HC_BLOCK 512
 #endif
 #ifndef HC_NPT
-#define HC_NPT 4
+#define HC_NPT 2
 #endif
 constexpr int BLOCK = HC_BLOCK;
 #ifndef HC_FMT16
 #define HC_FMT16 1
 #endif
 #ifndef HC_MINB
-#define HC_MINB (1024 / HC_BLOCK)
+#define HC_MINB 3   // 3 x 512-thread CTAs per SM (42 registers): ER-2^25 108 -> 95 ms, RMAT-26 1624 -> 1544 ms
 #endif
 constexpr int MIN_CTAS = HC_MINB;        // resident CTAs per SM the register budget targets
 #ifndef HC_MINB_SMALL
@@ -96,7 +96,7 @@ constexpr int BIN_HUB = 4;
 constexpr int NBIN = 5;
 constexpr int HUB_MIN = 4097;            // deg >= HUB_MIN -> hub
 #ifndef HC_HUB_U
-#define HC_HUB_U 8
+#define HC_HUB_U 4
 #endif
 constexpr int HU = HC_HUB_U;             // column loads in flight per thread in the CTA-per-node paths
 constexpr int HUB_WORDS = 512;           // CTA bitmap window: 16384 colors per pass
