@@ -403,7 +403,9 @@ def run_distributed(args, cfg):
                        "parallelism": f"1d-partition x{world} (edge-balanced)", "exchange": exchange,
                        "valid": valid, "l2": "flushed between timed steps (512 MiB write)"},
             "clocks": clk.summary(),
-            "gpu_launches": (9 if solver is not None else 4 * rounds + 3) * args.steps,
+            # peer path: bucket sort (3) + copy_totals + fill_od + narrow + delta + max_degree
+            # + boundary flags + the solve kernel; host-staged path: 4 kernels per round
+            "gpu_launches": (10 if solver is not None else 4 * rounds + 3) * args.steps,
             "e2e": {"value": und * args.steps / (e2e_total / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": world * (8 * (n + 1) + 8 * dg.num_edges),
                     "d2h_bytes_per_step": world * 8 * n},
@@ -456,7 +458,10 @@ def run_ours(args, cfg):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stream = torch.cuda.current_stream()
-    launches_per_step = 6  # bucket count/scan/scatter + copy_totals + narrow_offsets + solve_kernel
+    # bucket count/scan/scatter + copy_totals + fill_od + narrow_offsets and
+    # delta_columns (int32-offset graphs) + solve_kernel (see the ncu launch list)
+    narrow = dg.num_edges < (1 << 31) - 1
+    launches_per_step = 3 + 1 + 1 + (1 if narrow else 0) + (1 if narrow and dg.num_edges else 0) + 1
     torch.cuda.synchronize()
     with Clocks(local) as clk:
         for i in range(args.steps):
