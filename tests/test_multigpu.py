@@ -101,6 +101,21 @@ def test_partition_bounds_edge_balanced():
     assert partition_bounds(np.zeros(5, np.int64), 2) == [(0, 2), (2, 4)]
 
 
+def test_partition_bounds_device_form_matches_host():
+    """multigpu.partition_bounds_device (searchsorted on the row-offset tensor,
+    used by the peer-memory solve) == distributed.partition_bounds, on CPU
+    tensors here."""
+    from paper_1912_01478_b200.distributed import partition_bounds
+    from paper_1912_01478_b200.multigpu import partition_bounds_device
+
+    rng = np.random.default_rng(4)
+    graphs = [O.build_csr(1 << 10, O.gen_rmat(10, 16, 3))[0], O.build_csr(500, rng.integers(0, 500, (3000, 2)))[0],
+              np.zeros(8, np.int64), O.build_csr(30 * 20, O.gen_grid(30, 20))[0]]
+    for ro in graphs:
+        for world in (1, 2, 3, 5, 8):
+            assert partition_bounds_device(torch.from_numpy(ro), world) == partition_bounds(ro, world)
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_partitioned_solve_gloo_cpu(world):
     _run(world, use_gpu=False)
