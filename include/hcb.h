@@ -175,6 +175,12 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
 #define HC_IPC_HANDLE_BYTES 64
 size_t hc_mg_shared_bytes(int64_t num_nodes);
 size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t num_edges, int64_t lo, int64_t hi);
+/* The one allocation the library makes: a shared region in its own
+ * cudaMalloc allocation (zeroed), so it is IPC-exportable whatever the
+ * caller's allocator does (e.g. virtual-memory segments).  Freed by
+ * hc_mg_free_shared after every peer closed its mapping. */
+int hc_mg_alloc_shared(size_t bytes, void **h_dptr);
+int hc_mg_free_shared(void *d_ptr);
 /* export a device pointer for another process: cudaIpc handle of the
  * allocation that contains it + the pointer's offset in it */
 int hc_mg_ipc_export(const void *d_ptr, void *h_handle, int64_t *h_offset);

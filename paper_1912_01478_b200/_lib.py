@@ -79,6 +79,8 @@ _SIGS = {
     "hc_solve_stats": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, _p, ctypes.c_size_t, _p]),
     "hc_mg_shared_bytes": (ctypes.c_size_t, [_i64]),
     "hc_mg_workspace_bytes": (ctypes.c_size_t, [_i64, _i64, _i64, _i64]),
+    "hc_mg_alloc_shared": (ctypes.c_int, [ctypes.c_size_t, _p]),
+    "hc_mg_free_shared": (ctypes.c_int, [_p]),
     "hc_mg_ipc_export": (ctypes.c_int, [_p, _p, _p]),
     "hc_mg_ipc_import": (ctypes.c_int, [_p, _i64, _p]),
     "hc_mg_ipc_close": (ctypes.c_int, [_p, _i64]),

@@ -1432,22 +1432,21 @@ __global__ void narrow_offsets_kernel(const long long *ro, int *ro32, long long 
 }
 
 // int16 delta columns ci16[k] = ci[k] - u; sets *bad when some |v-u| >= 2^15
-// (then the absolute int32 columns are used).  Warp per row, early exit.
+// (then the absolute int32 columns are used).  Thread per row (rows that
+// qualify are short: grids, meshes), early exit at the first violation.
 __global__ void delta_columns_kernel(const long long *ro, const int *ci, long long lo, long long hi,
                                      short *ci16, unsigned *bad) {
-    const unsigned lane = lane_id();
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long u = lo + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < hi; u += nwarps) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long u = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; u < hi; u += stride) {
         if (*(volatile unsigned *)bad) return;
-        bool over = false;
-        for (long long k = ro[u] + lane; k < ro[u + 1]; k += 32) {
+        const long long e = ro[u + 1];
+        for (long long k = ro[u]; k < e; ++k) {
             const long long d = (long long)ci[k] - u;
-            over |= d < -32768 || d > 32767;
+            if (d < -32768 || d > 32767) {
+                atomicOr(bad, 1u);
+                return;
+            }
             ci16[k] = (short)d;
-        }
-        if (__any_sync(FULL, over)) {
-            if (lane == 0) atomicOr(bad, 1u);
-            return;
         }
     }
 }
@@ -1784,6 +1783,24 @@ size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t num_edges, int64_t lo, i
     const long long n = num_nodes < 0 ? 0 : num_nodes;
     const long long nown = hi > lo ? hi - lo : 0;
     return layout(n, num_edges < 0 ? 0 : num_edges, nown, true).total;
+}
+
+int hc_mg_alloc_shared(size_t bytes, void **h_dptr) {
+    HC_REQUIRE(h_dptr && bytes > 0, HC_ERR_INVALID, "hc_mg_alloc_shared: bad arguments");
+    void *p = nullptr;
+    HC_CUDA_TRY(cudaMalloc(&p, bytes));
+    const cudaError_t e = cudaMemset(p, 0, bytes);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        HC_CUDA_TRY(e);
+    }
+    *h_dptr = p;
+    return HC_OK;
+}
+
+int hc_mg_free_shared(void *d_ptr) {
+    if (d_ptr) HC_CUDA_TRY(cudaFree(d_ptr));
+    return HC_OK;
 }
 
 int hc_mg_ipc_export(const void *d_ptr, void *h_handle, int64_t *h_offset) {

@@ -136,8 +136,13 @@ class DeviceCsr:
             return self.host.max_degree
         if self.num_nodes == 0:
             return 0
-        ro = self.row_offsets.cpu().numpy()
-        return int(np.diff(ro).max())
+        L = _lib.load()  # device reduction (hc_degree_stats), no host copy of the offsets
+        ws = _lib.workspace(L.hc_degree_stats_workspace_bytes(), self.device)
+        lo, med, hi = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+        _lib.check(L.hc_degree_stats(self.row_offsets.data_ptr(), self.num_nodes, ctypes.byref(lo),
+                                     ctypes.byref(med), ctypes.byref(hi), ws.data_ptr(), ws.numel(),
+                                     _lib.stream_handle()))
+        return int(hi.value)
 
     @property
     def col_indices_i64(self) -> torch.Tensor:

@@ -213,11 +213,13 @@ class PeerGroup:
         self.rank = dist.get_rank(group)
         if self.world > MAX_WORLD:
             raise ValueError(f"world size {self.world} > {MAX_WORLD}")
-        self.region = torch.zeros(L.hc_mg_shared_bytes(num_nodes), dtype=torch.uint8, device=dev)
-        torch.cuda.synchronize()
+        # own cudaMalloc allocation: exportable whatever torch's allocator does
+        reg = ctypes.c_void_p(0)
+        _lib.check(L.hc_mg_alloc_shared(L.hc_mg_shared_bytes(num_nodes), ctypes.byref(reg)))
+        self.region_ptr = int(reg.value)
         handle = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
         off = ctypes.c_int64(0)
-        _lib.check(L.hc_mg_ipc_export(self.region.data_ptr(), handle, ctypes.byref(off)))
+        _lib.check(L.hc_mg_ipc_export(self.region_ptr, handle, ctypes.byref(off)))
         mine = (bytes(handle.raw), int(off.value))
         allinfo = [None] * self.world
         dist.all_gather_object(allinfo, mine, group=group)
@@ -226,7 +228,7 @@ class PeerGroup:
         try:
             for q, (h, o) in enumerate(allinfo):
                 if q == self.rank:
-                    self.ptrs.append(self.region.data_ptr())
+                    self.ptrs.append(self.region_ptr)
                     continue
                 p = ctypes.c_void_p(0)
                 _lib.check(L.hc_mg_ipc_import(ctypes.create_string_buffer(h, IPC_HANDLE_BYTES), o,
@@ -241,6 +243,9 @@ class PeerGroup:
             for p, o in self._opened:
                 L.hc_mg_ipc_close(ctypes.c_void_p(p), o)
             self._opened = []
+            dist.barrier(group=group)
+            L.hc_mg_free_shared(ctypes.c_void_p(self.region_ptr))
+            self.region_ptr = 0
             raise RuntimeError(f"peer mapping failed on ranks {[q for q, f in enumerate(flags) if not f]}: "
                                f"{err!r}")
 
@@ -252,6 +257,10 @@ class PeerGroup:
         for p, o in self._opened:
             _lib.check(self.L.hc_mg_ipc_close(ctypes.c_void_p(p), o))
         self._opened = []
+        dist.barrier(group=self.group)  # every peer unmapped this rank's region
+        if self.region_ptr:
+            _lib.check(self.L.hc_mg_free_shared(ctypes.c_void_p(self.region_ptr)))
+            self.region_ptr = 0
 
 
 class MgSolver:
