@@ -162,6 +162,9 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
 /* (|W'|, conflicts) for the identical hybrid decision on every rank    */
 /* (driver.py:145-152).  Colors, rounds and per-round records are       */
 /* bit-identical to hc_solve for every partition.                       */
+/*   h_bounds[world+1]: the partition (rank r owns [h_bounds[r],        */
+/*     h_bounds[r+1]); every rank passes the same array).  A boundary   */
+/*     word goes only to the ranks holding a neighbour of it.           */
 /*   hc_mg_solve: preprocessing (synchronous) + launch (asynchronous);  */
 /*     d_colors int64[hi-lo] receives the owned colors; every rank's    */
 /*     d_rec gets the same global records; ctas = 0: all resident CTAs; */
@@ -187,18 +190,22 @@ int hc_mg_ipc_export(const void *d_ptr, void *h_handle, int64_t *h_offset);
 int hc_mg_ipc_import(const void *h_handle, int64_t offset, void **h_dptr);
 int hc_mg_ipc_close(void *d_ptr, int64_t offset);
 int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
-                int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                 int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
                 int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
 /* hc_mg_solve == hc_mg_prepare + hc_mg_launch.  Ranks sharing one GPU
  * prepare all ranks first, then launch all (preprocessing kernels must not
  * queue behind another rank's persistent kernel). */
 int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
-                  int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                  int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                   int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
                   int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
 int hc_mg_launch(void *d_ws, void *stream);
 int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream);
+/* How a rank's boundary words reach its peers (process-wide; tests /
+ * experiments): 0 = per round, the cheaper of (1) mirroring every boundary
+ * store and (2) copying the boundary zones at the end of each phase. */
+int hc_mg_set_exchange(int mode);
 
 /* ------------------------------------------------------------------ */
 /* 1D-partitioned multi-GPU solve: per-phase kernels  */

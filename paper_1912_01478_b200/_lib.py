@@ -84,10 +84,11 @@ _SIGS = {
     "hc_mg_ipc_export": (ctypes.c_int, [_p, _p, _p]),
     "hc_mg_ipc_import": (ctypes.c_int, [_p, _i64, _p]),
     "hc_mg_ipc_close": (ctypes.c_int, [_p, _i64]),
-    "hc_mg_solve": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
+    "hc_mg_solve": (ctypes.c_int, [_p, _p, _i64, _i64, _p, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
                                    _i64, _p, _p, _i64, ctypes.c_int, _i64, _p, ctypes.c_size_t, _p]),
     "hc_mg_wait": (ctypes.c_int, [_p, _p, _p]),
-    "hc_mg_prepare": (ctypes.c_int, [_p, _p, _i64, _i64, _i64, _i64, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
+    "hc_mg_set_exchange": (ctypes.c_int, [ctypes.c_int]),
+    "hc_mg_prepare": (ctypes.c_int, [_p, _p, _i64, _i64, _p, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
                                      _i64, _p, _p, _i64, ctypes.c_int, _i64, _p, ctypes.c_size_t, _p]),
     "hc_mg_launch": (ctypes.c_int, [_p, _p]),
     "hc_dist_boundary": (ctypes.c_int, [_p, _p, _i64, _i64, _p, _p]),

@@ -86,6 +86,9 @@ constexpr int MIN_CTAS = HC_MINB;        // resident CTAs per SM the register bu
 constexpr int MIN_CTAS_SMALL = HC_MINB_SMALL;  // the same for bin-0-only graphs (SmemT<true>)
 constexpr int NW = BLOCK / 32;
 constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
+#ifndef HC_MG_PLAIN_BARRIER
+#define HC_MG_PLAIN_BARRIER 0
+#endif
 #ifndef HC_NPT_SMALL
 #define HC_NPT_SMALL 2
 #endif
@@ -186,12 +189,15 @@ struct Params {
     unsigned *fmt_overflow;    // set when a tentative color does not fit the state word
     long long lo, nown;        // owned node range [lo, lo + nown) (single GPU: 0, n)
     // multi-GPU (Fmt::mg) only
-    const unsigned char *bnd;  // boundary flag, indexed by global node id (owned ids only)
+    const unsigned char *bnd;  // per owned node: bit q = rank q reads this word (global id index)
+    long long zlo, zhi;        // boundary zones: nodes u with u - lo < zlo or hi - u <= zhi may be read by peers
+    long long peer_words;      // sum over owned nodes of the peers reading them (mirror cost model)
     void *const *peer_x;       // [world] every rank's state-word replica (device array)
     Mbox *const *peer_mbox;    // [world] every rank's mailbox
     Mbox *mbox;                // this rank's mailbox
     int rank, world;
     long long timeout_ns;      // cross-GPU barrier wait limit
+    int exchange;              // 0 auto (per round), 1 always mirror stores, 2 always zone copies
 };
 
 // A bin's current list: dense (static list / round 1) or segmented (the
@@ -217,6 +223,7 @@ struct RoundCfg {
     unsigned hub_split;            // hubs split into equal-size edge slices (latency regime)
     unsigned hub_slice;            // edges per slice
     bool topo, ident, bin3_by_cta, ident_small;
+    bool bulk;                     // multi-GPU: this round's words go to the peers by zone copies
 };
 
 // SMALL: the graph has only bin-0 nodes (max degree <= 16: grids, meshes,
@@ -312,6 +319,9 @@ __device__ __forceinline__ void seg_put(const Params &P, int np, int bin, unsign
 // set by any thread of the CTA that issued NVLink stores in the current
 // phase: only such CTAs need the system-scope fence before the next barrier
 __shared__ unsigned s_mirrored;
+// multi-GPU, per round: the boundary zones are copied to the peers at the end
+// of each phase instead of mirroring every store (dense boundaries)
+__shared__ unsigned s_bulk;
 
 // Cross-GPU barrier of the multi-GPU solve: the grid barrier whose last
 // arriving CTA exchanges (epoch, payload) with every rank's mailbox over
@@ -344,6 +354,12 @@ __device__ bool mg_sync(const Params &P, SMT &sm, unsigned long long epoch, int 
                 a = __ldcg(&C->wl_next[p ^ 1]) + __ldcg(&C->hub_cnt[p ^ 1]);
                 c = __ldcg(&C->conflicts[p]);
             }
+            unsigned long long sa = 0, sc = 0;
+            unsigned ok = 1;
+#if HC_MG_PLAIN_BARRIER  // experiment knob (valid for one rank only): no mailbox, no system fences
+            sa = a;
+            sc = c;
+#else
             // release: everything this GPU wrote (observed through the
             // arrivals) before the tags; then relaxed tagged stores
             fence_acq_rel_sys();
@@ -356,8 +372,6 @@ __device__ bool mg_sync(const Params &P, SMT &sm, unsigned long long epoch, int 
                 for (int w = 0; w < 3; ++w) st_relaxed_sys_u64(&sl->w[w], wv[w]);
             }
             const unsigned long long t0 = globaltimer();
-            unsigned long long sa = 0, sc = 0;
-            unsigned ok = 1;
             for (int q = 0; q < P.world && ok; ++q) {
                 MboxSlot *sl = &P.mbox->slot[par][q];
 #pragma unroll 1
@@ -377,6 +391,7 @@ __device__ bool mg_sync(const Params &P, SMT &sm, unsigned long long epoch, int 
                 }
             }
             fence_acq_rel_sys();  // acquire: the peers' data before the tags they posted
+#endif
             if (!ok) C->abort = 1u;
             if (kind == 1) {
                 C->g_wl = sa;
@@ -446,21 +461,61 @@ __device__ __forceinline__ void xraw(const Params &P, long long v, unsigned w) {
 // multi-GPU: the word of an owned boundary node is also stored into every
 // peer's replica (NVLink stores; made visible by the fence.sys of the next
 // cross-GPU barrier).  Interior words are read by no other rank.
+// Only the ranks that read the word get it (bit q of the node's peer mask),
+// and the mask is loaded only inside the boundary zones at the two ends of
+// the owned range (an arithmetic test; grids: a few rows per cut).
 template <class F>
-__device__ __forceinline__ void mirror(const Params &P, long long v, unsigned w) {
+__device__ __forceinline__ void mirror(const Params &P, long long v, unsigned w, unsigned mask) {
     s_mirrored = 1u;
-    for (int q = 0; q < P.world; ++q)
-        if (q != P.rank)
-            reinterpret_cast<typename F::xt *>(__ldg(reinterpret_cast<const unsigned long long *>(P.peer_x) + q))[v] =
-                (typename F::xt)w;
+    while (mask) {
+        const int q = __ffs(mask) - 1;
+        mask &= mask - 1u;
+        reinterpret_cast<typename F::xt *>(__ldg(reinterpret_cast<const unsigned long long *>(P.peer_x) + q))[v] =
+            (typename F::xt)w;
+    }
 }
 template <class F>
 __device__ __forceinline__ void xput(const Params &P, long long v, unsigned w) {
     reinterpret_cast<typename F::xt *>(P.X)[v] = (typename F::xt)w;
     if constexpr (F::mg) {
-        if (__ldg(P.bnd + v)) mirror<F>(P, v, w);
+        if (!s_bulk && (v - P.lo < P.zlo || P.lo + P.nown - v <= P.zhi)) {
+            const unsigned mask = __ldg(P.bnd + v);
+            if (mask) mirror<F>(P, v, w, mask);
+        }
     }
 }
+// Zone copy (bulk exchange): the prefix [lo, lo+zlo) goes to every lower rank
+// and the suffix [hi-zhi, hi) to every higher rank -- every word a peer can
+// read lies there (mg_boundary_kernel).  All CTAs, 16-byte vector stores.
+template <class F>
+__device__ void zone_copy(const Params &P) {
+    using xt = typename F::xt;
+    constexpr long long V = 16 / sizeof(xt);  // words per vector
+    const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long gthreads = (long long)P.nblocks * blockDim.x;
+    const xt *src = reinterpret_cast<const xt *>(P.X);
+    bool any = false;
+    for (int q = 0; q < P.world; ++q) {
+        if (q == P.rank) continue;
+        const long long b = q < P.rank ? P.lo : P.lo + P.nown - P.zhi;
+        const long long e = q < P.rank ? P.lo + P.zlo : P.lo + P.nown;
+        if (e <= b) continue;
+        any = true;
+        xt *dst = reinterpret_cast<xt *>(__ldg(reinterpret_cast<const unsigned long long *>(P.peer_x) + q));
+        const long long vb = (b + V - 1) / V, ve = e / V;  // whole vectors inside [b, e)
+        if (vb < ve) {
+            for (long long i = b + gtid; i < vb * V; i += gthreads) dst[i] = src[i];
+            for (long long i = ve * V + gtid; i < e; i += gthreads) dst[i] = src[i];
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+            uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+            for (long long i = vb + gtid; i < ve; i += gthreads) d4[i] = __ldcg(s4 + i);
+        } else {
+            for (long long i = b + gtid; i < e; i += gthreads) dst[i] = src[i];
+        }
+    }
+    if (any) s_mirrored = 1u;
+}
+
 // tentative color write: a 16-bit word cannot hold T > 32767 (possible only
 // for degree > 32766); flag it, the host reruns the solve with 32-bit words
 template <class F>
@@ -1185,6 +1240,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         if (threadIdx.x == 0) {
             s_mirrored = 0u;
             s_wl_acc = 0ull;
+            s_bulk = 0u;
         }
         ep = *(volatile unsigned long long *)&P.mbox->last_epoch;
         if (!mg_sync(P, sm, ++ep, 0, 0)) return;
@@ -1267,6 +1323,17 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                     rc.L[b] = List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false};
             rc.topo = topo;
             rc.ident = topo && rc.ident_small;
+            if constexpr (F::mg) {
+                // bulk when copying the zones (plus the extra local barrier it
+                // needs, ~2 MB of link time) is cheaper than mirroring the
+                // expected boundary stores of the round (~32 B per scattered
+                // peer store; the active set is assumed boundary-proportional)
+                const double zbytes =
+                    ((double)P.zlo * P.rank + (double)P.zhi * (P.world - 1 - P.rank)) * sizeof(typename F::xt);
+                const double mbytes = (double)s * (double)P.peer_words / (double)max(P.nown, 1LL) * 32.0;
+                rc.bulk = P.world > 1 && (P.exchange == 2 || (P.exchange == 0 && zbytes + 2097152.0 < mbytes));
+                s_bulk = rc.bulk ? 1u : 0u;
+            }
             rc.csz[0] = chunk_size(rc.L[0].total, BLOCK * (F::small ? NPT_SMALL : NPT));
             rc.csz[1] = chunk_size(rc.L[1].total, NW * 4);
             rc.csz[2] = chunk_size(rc.L[2].total, NW * 2);
@@ -1346,6 +1413,10 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
 
         run_phase<OffT, F, STATS, 0>(P, ro, sm, p, my_conf, my_edges);
         if constexpr (F::mg) {
+            if (rc.bulk) {  // every local word of the phase written, then the zones go out
+                grid_sync(&C->bar, P.nblocks);
+                zone_copy<F>(P);
+            }
             if (!mg_sync(P, sm, ++ep, 0, p)) return;  // peers' tentative colors are in
         } else {
             grid_sync(&C->bar, P.nblocks);
@@ -1380,6 +1451,10 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                 rc.prev_cap[b] = rc.csz[b];
             }
         if constexpr (F::mg) {
+            if (rc.bulk) {
+                grid_sync(&C->bar, P.nblocks);
+                zone_copy<F>(P);
+            }
             if (!mg_sync(P, sm, ++ep, 1, p)) return;  // winners in; global (|W'|, conflicts)
         } else {
             grid_sync(&C->bar, P.nblocks);
@@ -1473,6 +1548,37 @@ __global__ void max_degree_kernel(const long long *ro, long long n, unsigned lon
     if (lane_id() == 0 && d) atomicMax(out, d);
 }
 
+// multi-GPU: per owned node the mask of the ranks holding a neighbour, and the
+// boundary zones (longest prefix / suffix of the owned range that contains a
+// node read by a lower / higher rank).  Warp per node.
+__global__ void mg_boundary_kernel(const long long *ro, const int *ci, const long long *bounds, int world,
+                                   int rank, unsigned char *mask, unsigned long long *zones) {
+    __shared__ long long sb[MG_MAX_WORLD + 1];
+    if (threadIdx.x <= (unsigned)world) sb[threadIdx.x] = bounds[threadIdx.x];
+    __syncthreads();
+    const long long lo = sb[rank], hi = sb[rank + 1];
+    const unsigned lane = lane_id();
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long u = lo + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < hi; u += nwarps) {
+        unsigned m = 0;
+        for (long long k = ro[u] + lane; k < ro[u + 1]; k += 32) {
+            const long long v = ci[k];
+            if (v >= lo && v < hi) continue;
+            int q = 0;
+            while (q + 1 < world && v >= sb[q + 1]) ++q;
+            m |= 1u << q;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m |= __shfl_xor_sync(FULL, m, o);
+        if (lane == 0) {
+            mask[u - lo] = (unsigned char)m;
+            if (m) atomicAdd(&zones[2], (unsigned long long)__popc(m));
+            if (m & ((1u << rank) - 1u)) atomicMax(&zones[0], (unsigned long long)(u - lo + 1));
+            if (m >> (rank + 1)) atomicMax(&zones[1], (unsigned long long)(hi - u));
+        }
+    }
+}
+
 // worst-case segmented capacity of a bin with `cnt` static nodes
 inline size_t seg_capacity(long long cnt) {
     return (size_t)cnt + (size_t)cnt / MAXSEG + 2 * BLOCK * NPT;
@@ -1510,7 +1616,7 @@ static Layout layout(long long n, long long m, long long nown, bool mg) {
     L.hub_acc = o; o = align_up(o + sizeof(HubAcc) * MAX_SPLIT_SLOTS, 256);
     L.part = o; o = align_up(o + part_scratch_bytes(NKEY, nown), 256);
     L.bnd = o; o = align_up(o + (mg ? (size_t)nown : 0), 256);
-    L.ptrs = o; o = align_up(o + (mg ? 2 * sizeof(void *) * MG_MAX_WORLD : 0), 256);
+    L.ptrs = o; o = align_up(o + (mg ? 2 * sizeof(void *) * MG_MAX_WORLD + 8 * (MG_MAX_WORLD + 1) + 24 : 0), 256);
     L.maxdeg = o; o = align_up(o + 8, 256);
     L.total = o;
     return L;
@@ -1563,7 +1669,7 @@ static int occupancy() {
 
 // format overrides (tests / experiments): force int64 offsets, forbid the
 // 16-bit state word, forbid 16-bit delta columns
-static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0;
+static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0, g_mg_exchange = 0;
 
 // Per-solve preprocessing shared by hc_solve and hc_mg_solve, for the owned
 // range [lo, lo + nown): fresh control block, static degree-bucketed lists,
@@ -1672,6 +1778,12 @@ int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16) {
     g_force_wide = force_wide_offsets;
     g_no_x16 = no_x16;
     g_no_c16 = no_c16;
+    return HC_OK;
+}
+
+int hc_mg_set_exchange(int mode) {
+    HC_REQUIRE(mode >= 0 && mode <= 2, HC_ERR_INVALID, "hc_mg_set_exchange: mode %d invalid", mode);
+    g_mg_exchange = mode;
     return HC_OK;
 }
 
@@ -1836,9 +1948,16 @@ int hc_mg_ipc_close(void *d_ptr, int64_t offset) {
 }
 
 int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
-                  int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                  int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                   int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
                   int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
+    HC_REQUIRE(h_bounds && world >= 1 && world <= MG_MAX_WORLD && rank >= 0 && rank < world, HC_ERR_INVALID,
+               "hc_mg_solve: rank %d / world %d invalid (world <= %d)", rank, world, MG_MAX_WORLD);
+    for (int q = 0; q < world; ++q)
+        HC_REQUIRE(h_bounds[q] <= h_bounds[q + 1], HC_ERR_INVALID, "hc_mg_solve: bounds not ascending");
+    HC_REQUIRE(h_bounds[0] == 0 && h_bounds[world] == num_nodes, HC_ERR_INVALID,
+               "hc_mg_solve: bounds must cover [0, num_nodes)");
+    const int64_t lo = h_bounds[rank], hi = h_bounds[rank + 1];
     HC_REQUIRE(num_nodes >= 1 && num_nodes < 0x7fffffffLL, HC_ERR_INVALID,
                "hc_mg_solve: num_nodes %lld out of range", (long long)num_nodes);
     HC_REQUIRE(num_edges >= 0, HC_ERR_INVALID, "hc_mg_solve: num_edges < 0");
@@ -1869,13 +1988,26 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
     P.rank = rank;
     P.world = world;
     P.timeout_ns = (timeout_ms > 0 ? timeout_ms : 60000) * 1000000LL;
+    P.exchange = g_mg_exchange;
     Prep pr;
     int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, true, pr, st);
     if (rc != HC_OK) return rc;
-    // boundary flags of the owned nodes (a neighbour outside [lo, hi))
+    // peer masks of the owned nodes + boundary zones
     unsigned char *bnd = reinterpret_cast<unsigned char *>(ws + L.bnd);
-    rc = hc_dist_boundary(d_row_offsets, d_col_indices, lo, hi, bnd, stream);
-    if (rc != HC_OK) return rc;
+    long long *d_bounds = reinterpret_cast<long long *>(ws + L.ptrs + 2 * sizeof(void *) * MG_MAX_WORLD);
+    unsigned long long *d_zones = reinterpret_cast<unsigned long long *>(d_bounds + MG_MAX_WORLD + 1);
+    long long hb[MG_MAX_WORLD + 1] = {};
+    for (int q = 0; q <= world; ++q) hb[q] = h_bounds[q];
+    HC_CUDA_TRY(cudaMemcpyAsync(d_bounds, hb, sizeof hb, cudaMemcpyHostToDevice, st));
+    HC_CUDA_TRY(cudaMemsetAsync(d_zones, 0, 24, st));
+    if (hi > lo && num_edges > 0) {
+        const long long blocks = std::min<long long>((hi - lo + 7) / 8, (long long)std::max(1, num_sms()) * 16);
+        mg_boundary_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long *>(d_row_offsets),
+                                                              d_col_indices, d_bounds, world, rank, bnd, d_zones);
+        HC_CHECK_LAUNCH();
+    }
+    unsigned long long hz[3] = {0, 0, 0};
+    HC_CUDA_TRY(cudaMemcpyAsync(hz, d_zones, sizeof hz, cudaMemcpyDeviceToHost, st));
     P.bnd = bnd - lo;
     // peer tables: every rank's replica and mailbox (pointers valid in this process)
     void *tab[2 * MG_MAX_WORLD] = {};
@@ -1886,6 +2018,9 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
     void **d_tab = reinterpret_cast<void **>(ws + L.ptrs);
     HC_CUDA_TRY(cudaMemcpyAsync(d_tab, tab, sizeof tab, cudaMemcpyHostToDevice, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
+    P.zlo = (long long)hz[0];
+    P.zhi = (long long)hz[1];
+    P.peer_words = (long long)hz[2];
     P.peer_x = d_tab;
     P.peer_mbox = reinterpret_cast<Mbox *const *>(d_tab + MG_MAX_WORLD);
     P.X = h_shared[rank];
@@ -1924,10 +2059,10 @@ int hc_mg_launch(void *d_ws, void *stream) {
 }
 
 int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
-                int64_t num_edges, int64_t lo, int64_t hi, int rank, int world, void *const *h_shared,
+                int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                 int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
                 int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
-    const int rc = hc_mg_prepare(d_row_offsets, d_col_indices, num_nodes, num_edges, lo, hi, rank, world,
+    const int rc = hc_mg_prepare(d_row_offsets, d_col_indices, num_nodes, num_edges, h_bounds, rank, world,
                                  h_shared, mode, thr_count, d_colors, d_rec, max_rec, ctas, timeout_ms, d_ws,
                                  ws_bytes, stream);
     return rc != HC_OK ? rc : hc_mg_launch(d_ws, stream);

@@ -68,14 +68,16 @@ class RankSolver:
     """One rank's reusable solve state for the owned range [lo, hi):
     workspace, owned colors and the (global) per-round records."""
 
-    def __init__(self, graph: DeviceCsr, lo: int, hi: int, rank: int, world: int,
+    def __init__(self, graph: DeviceCsr, bounds: list[tuple[int, int]], rank: int, world: int,
                  shared_ptrs: list[int], *, max_rec: int | None = None, ctas: int = 0,
                  timeout_ms: int = 60000):
         if not 1 <= world <= MAX_WORLD:
             raise ValueError(f"world size {world} not in [1, {MAX_WORLD}]")
         self.L = _lib.load()
         self.g = graph
+        lo, hi = bounds[rank]
         self.lo, self.hi, self.rank, self.world = int(lo), int(hi), int(rank), int(world)
+        self.cuts = (ctypes.c_int64 * (world + 1))(*([b[0] for b in bounds] + [bounds[-1][1]]))
         dev = graph.device
         n = graph.num_nodes
         self.ws = _lib.workspace(self.L.hc_mg_workspace_bytes(n, graph.num_edges, self.lo, self.hi), dev)
@@ -95,7 +97,7 @@ class RankSolver:
         g = self.g
         _lib.check(self.L.hc_mg_prepare(
             g.row_offsets.data_ptr(), _lib.ptr(g.col_indices), g.num_nodes, g.num_edges,
-            self.lo, self.hi, self.rank, self.world, ctypes.cast(self.shared, ctypes.c_void_p),
+            ctypes.cast(self.cuts, ctypes.c_void_p), self.rank, self.world, ctypes.cast(self.shared, ctypes.c_void_p),
             _lib.MODE_CODES[mode], int(thr_count),
             self.colors.data_ptr(), self.rec.data_ptr(), self.max_rec, self.ctas, self.timeout_ms,
             self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(stream)))
@@ -153,8 +155,8 @@ class VirtualMesh:
                         for _ in range(world)]
         ptrs = [r.data_ptr() for r in self.regions]
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
-        self.ranks = [RankSolver(graph, lo, hi, p, world, ptrs, ctas=ctas, timeout_ms=timeout_ms)
-                      for p, (lo, hi) in enumerate(self.bounds)]
+        self.ranks = [RankSolver(graph, self.bounds, p, world, ptrs, ctas=ctas, timeout_ms=timeout_ms)
+                      for p in range(world)]
         torch.cuda.synchronize()
 
     def solve(self, mode: str, thr_count: int):
@@ -273,8 +275,7 @@ class MgSolver:
         self.group = group
         self.world, self.rank = self.peers.world, self.peers.rank
         self.bounds = partition_bounds_device(graph.row_offsets, self.world)
-        lo, hi = self.bounds[self.rank]
-        self.rs = RankSolver(graph, lo, hi, self.rank, self.world, self.peers.ptrs, timeout_ms=timeout_ms)
+        self.rs = RankSolver(graph, self.bounds, self.rank, self.world, self.peers.ptrs, timeout_ms=timeout_ms)
         self.mx = max(h - l for l, h in self.bounds)
         self.start = torch.cuda.Event(enable_timing=True)
         self.stop = torch.cuda.Event(enable_timing=True)

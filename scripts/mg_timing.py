@@ -25,7 +25,7 @@ for name in sys.argv[1:] or ["grid4096", "rmat22"]:
     single = min(s.run("hybrid", thr, fetch_records=False).seconds for _ in range(3))
     want = s.run("hybrid", thr).colors.cpu().numpy()
     row = {"single_ms": single * 1e3}
-    for world in (1, 2, 4, 8):
+    for world in [int(w) for w in __import__("os").environ.get("WORLDS", "1,2,4,8").split(",")]:
         mesh = VirtualMesh(dg, world, timeout_ms=60000)
         virtual_color_graph(dg, cfg, world, mesh=mesh)
         ts = []

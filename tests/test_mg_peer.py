@@ -107,6 +107,23 @@ def test_virtual_ranks_hub_graph_and_formats():
         _lib.load().hc_solve_set_formats(0, 0, 0)
 
 
+@pytest.mark.parametrize("exchange", [1, 2])
+def test_virtual_ranks_forced_exchange_modes(exchange):
+    """Mirrored stores only (1) and zone copies only (2), each alone, must
+    reproduce the single-GPU solve (auto mode mixes them per round)."""
+    L = _lib.load()
+    L.hc_mg_set_exchange(exchange)
+    try:
+        graphs = [G.build_csr_device(G.gen_rmat_edges(11, 16, 5), 1 << 11), G.grid_graph(70, 50),
+                  G.build_csr_device(G.gen_er_edges(3000, 3000 * 12, 8), 3000)]
+        for dg in graphs:
+            for world in (2, 3, 5):
+                for mode in MODES:
+                    _check(dg, world, mode, 0.6)
+    finally:
+        L.hc_mg_set_exchange(0)
+
+
 def test_virtual_ranks_repeated_solves_and_empty_ranges():
     # barrier epochs continue across solves on the same mesh
     dg = G.build_csr_device(G.gen_rmat_edges(10, 16, 4), 1 << 10)
