@@ -28,3 +28,27 @@ hc.data_driven_iteration(g, state, wl, 1)
 hc.topology_driven_iteration(g, state, wl, 2)
 run_push_bench(5000, BenchConfig(batch_size=300, repetitions=1))
 print("sanitize workload ok")
+
+# bin-0-only kernel on a delta-column grid, multi-GPU virtual ranks (both
+# exchange modes), device MatrixMarket parse and degree statistics
+from paper_1912_01478_b200 import _lib
+from paper_1912_01478_b200.multigpu import virtual_color_graph
+
+import os
+
+dg = hc.grid_graph(50, 37)
+want, _ = hc.color_graph(dg)
+# virtual ranks need their persistent kernels to run concurrently, which the
+# sanitizers serialize: only world = 1 there unless SANITIZE_MG=1
+worlds = (2, 3) if os.environ.get("SANITIZE_MG") == "1" else (1,)
+for ex in (0, 1, 2):
+    _lib.load().hc_mg_set_exchange(ex)
+    for world in worlds:
+        r = virtual_color_graph(dg, hc.HybridConfig(), world, timeout_ms=120000)
+        assert np.array_equal(r.colors, want)
+    r = virtual_color_graph(hc.rmat_graph(9, 16, 2), hc.HybridConfig(), worlds[-1], timeout_ms=120000)
+_lib.load().hc_mg_set_exchange(0)
+el = hc.parse_matrix_market("%%MatrixMarket matrix coordinate pattern general\n4 4 3\n1 2\n% c\n3 4 7\n\n2 3\n")
+assert el.edges.tolist() == [[0, 1], [2, 3], [1, 2]]
+s = hc.degree_stats(hc.rmat_graph(10, 16, 3))
+print("sanitize workload ok (incl. multi-GPU + ingestion)")
