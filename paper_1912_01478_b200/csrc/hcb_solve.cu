@@ -686,10 +686,21 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
         if (threadIdx.x == 0) sm.hub_first = 0x7fffffff;
         __syncthreads();
         const unsigned hi = min(lim, w0 + HUB_WORDS * 32);
-        for (long long k = b + threadIdx.x; k < e; k += HU * BLOCK) {
-            int v[HU];
+        // software pipeline: the column ids of the next iteration are in
+        // flight while this iteration's neighbour words are gathered
+        int v[HU];
 #pragma unroll
-            for (int q = 0; q < HU; ++q) v[q] = (k + q * BLOCK < e) ? colget<F, true>(P, k + q * BLOCK, u) : -1;
+        for (int q = 0; q < HU; ++q) {
+            const long long k = b + threadIdx.x + q * BLOCK;
+            v[q] = k < e ? colget<F, true>(P, k, u) : -1;
+        }
+        for (long long k = b + threadIdx.x; k < e; k += HU * BLOCK) {
+            int nv[HU];
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                const long long kn = k + (HU + q) * BLOCK;
+                nv[q] = kn < e ? colget<F, true>(P, kn, u) : -1;
+            }
             unsigned x[HU];
 #pragma unroll
             for (int q = 0; q < HU; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
@@ -698,6 +709,8 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
                 const unsigned c = x[q] & CM<F>;
                 if ((x[q] & FB<F>) && c > w0 && c <= hi) mark(sm.hub_bm, c - w0);
             }
+#pragma unroll
+            for (int q = 0; q < HU; ++q) v[q] = nv[q];
         }
         __syncthreads();
         for (int i = threadIdx.x; i < HUB_WORDS; i += BLOCK)
@@ -721,12 +734,22 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
     if (threadIdx.x == 0) sm.red = 0;
     __syncthreads();
     unsigned cnt = 0, low = 0;
+    // software pipeline: the next chunk's column ids are in flight while
+    // this chunk's words are gathered (the adjacency is sorted, so the scan
+    // stops at the first chunk holding an id >= u)
+    int v[HU];
+#pragma unroll
+    for (int q = 0; q < HU; ++q) {
+        const long long k = b + (long long)warp * (32 * HU) + 32 * q + lane;
+        v[q] = k < e ? colget<F, true>(P, k, u) : 0x7fffffff;
+    }
     for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
-        int v[HU];
+        const bool more = __all_sync(FULL, v[HU - 1] < u);  // this chunk is wholly below u
+        int nv[HU];
 #pragma unroll
         for (int q = 0; q < HU; ++q) {
-            const long long k = k0 + 32 * q + lane;
-            v[q] = k < e ? colget<F, true>(P, k, u) : 0x7fffffff;
+            const long long k = k0 + 32LL * HU * NW + 32 * q + lane;
+            nv[q] = (more && k < e) ? colget<F, true>(P, k, u) : 0x7fffffff;
         }
         unsigned x[HU];
 #pragma unroll
@@ -737,6 +760,8 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
             if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
             else stop = true;
         }
+#pragma unroll
+        for (int q = 0; q < HU; ++q) v[q] = nv[q];
         if (__any_sync(FULL, stop)) break;  // later chunks are all >= u
     }
     cnt = warp_sum(cnt);
@@ -918,10 +943,19 @@ __device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigne
     for (int i = threadIdx.x; i < HA_WORDS + 2; i += BLOCK) sm.hub_bm[i] = 0u;  // [0,1]: mask, [2..]: words
     __syncthreads();
     unsigned long long mask = 0;
-    for (long long kk = b + threadIdx.x; kk < e; kk += HU * BLOCK) {
-        int v[HU];
+    int v[HU];  // software pipeline as in assign_cta
 #pragma unroll
-        for (int q = 0; q < HU; ++q) v[q] = (kk + q * BLOCK < e) ? colget<F, true>(P, kk + q * BLOCK, u) : -1;
+    for (int q = 0; q < HU; ++q) {
+        const long long kk = b + threadIdx.x + q * BLOCK;
+        v[q] = kk < e ? colget<F, true>(P, kk, u) : -1;
+    }
+    for (long long kk = b + threadIdx.x; kk < e; kk += HU * BLOCK) {
+        int nv[HU];
+#pragma unroll
+        for (int q = 0; q < HU; ++q) {
+            const long long kn = kk + (HU + q) * BLOCK;
+            nv[q] = kn < e ? colget<F, true>(P, kn, u) : -1;
+        }
         unsigned x[HU];
 #pragma unroll
         for (int q = 0; q < HU; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : 0u;
@@ -932,6 +966,8 @@ __device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigne
             if (c <= 64u) mask |= 1ull << (c - 1u);
             else if (c <= 64u + 32u * HA_WORDS) mark(sm.hub_bm + 2, c - 64u);
         }
+#pragma unroll
+        for (int q = 0; q < HU; ++q) v[q] = nv[q];
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mask |= __shfl_xor_sync(FULL, mask, o);
@@ -987,12 +1023,22 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
     const long long b = b0 + len * slice / k, e = b0 + len * (slice + 1) / k;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     unsigned cnt = 0, low = 0;
+    // software pipeline: the next chunk's column ids are in flight while
+    // this chunk's words are gathered (the adjacency is sorted, so the scan
+    // stops at the first chunk holding an id >= u)
+    int v[HU];
+#pragma unroll
+    for (int q = 0; q < HU; ++q) {
+        const long long kk = b + (long long)warp * (32 * HU) + 32 * q + lane;
+        v[q] = kk < e ? colget<F, true>(P, kk, u) : 0x7fffffff;
+    }
     for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
-        int v[HU];
+        const bool more = __all_sync(FULL, v[HU - 1] < u);  // this chunk is wholly below u
+        int nv[HU];
 #pragma unroll
         for (int q = 0; q < HU; ++q) {
-            const long long kk = k0 + 32 * q + lane;
-            v[q] = kk < e ? colget<F, true>(P, kk, u) : 0x7fffffff;
+            const long long kk = k0 + 32LL * HU * NW + 32 * q + lane;
+            nv[q] = (more && kk < e) ? colget<F, true>(P, kk, u) : 0x7fffffff;
         }
         unsigned x[HU];
 #pragma unroll
@@ -1003,6 +1049,8 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
             if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
             else stop = true;
         }
+#pragma unroll
+        for (int q = 0; q < HU; ++q) v[q] = nv[q];
         if (__any_sync(FULL, stop)) break;  // adjacency sorted: the rest is >= u
     }
     cnt = warp_sum(cnt);
