@@ -241,7 +241,11 @@ def color_graph(
     report.total_rounds = res.rounds
     report.colors_used = _colors_used_device(res.colors)
     report.valid = _verify_device(dg, res.colors) == 0
-    colors = res.colors.cpu().numpy().astype(np.int64, copy=False)
+    # D2H into page-locked memory (straight DMA; torch caches the pinned block)
+    host = torch.empty(res.colors.shape, dtype=torch.int64, pin_memory=True)
+    host.copy_(res.colors, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    colors = host.numpy()
     return colors, report
 
 
