@@ -573,12 +573,17 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
                                            const unsigned *prefix, unsigned long long v0,
                                            unsigned long long hi, bool topo, int *out,
                                            unsigned long long *out_od, unsigned *out_cnt, unsigned *bm,
+                                           unsigned &seg_hint,
                                            unsigned long long &my_conf, unsigned long long *my_edges) {
     const unsigned lane = lane_id();
     const unsigned sub = lane % G, gi = lane / G;
     const unsigned long long v = v0 + gi;
     // the list entry carries the adjacency range (no dependent row-offset load)
-    const long long idx = v < hi ? list_index(L, prefix, v) : -1;
+    // segment walk from the warp's hint (positions only grow along a chunk):
+    // no per-node binary search over up to MAXSEG segment starts
+    unsigned sg = seg_hint;
+    const long long idx = v < hi ? list_index_walk(L, prefix, v, sg) : -1;
+    seg_hint = __shfl_sync(FULL, sg, 0);  // lane 0 holds the tile's first (smallest) position
     int u = idx >= 0 ? ld_entry(L.base + idx) : -1;
     const unsigned long long od = idx >= 0 ? ld_od(L.od + idx) : 0ull;
     unsigned xu = 0;
@@ -694,6 +699,10 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
             const long long k = b + threadIdx.x + q * BLOCK;
             v[q] = k < e ? colget<F, true>(P, k, u) : -1;
         }
+        // colors w0+1 .. w0+64 (the common ones) go to a register mask,
+        // OR-reduced per warp: one shared atomic per warp instead of one per
+        // neighbour on the same few hot words
+        unsigned long long low = 0;
         for (long long k = b + threadIdx.x; k < e; k += HU * BLOCK) {
             int nv[HU];
 #pragma unroll
@@ -707,10 +716,18 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
 #pragma unroll
             for (int q = 0; q < HU; ++q) {
                 const unsigned c = x[q] & CM<F>;
-                if ((x[q] & FB<F>) && c > w0 && c <= hi) mark(sm.hub_bm, c - w0);
+                if (!(x[q] & FB<F>) || c <= w0 || c > hi) continue;
+                if (c <= w0 + 64u) low |= 1ull << (c - w0 - 1u);
+                else mark(sm.hub_bm, c - w0);
             }
 #pragma unroll
             for (int q = 0; q < HU; ++q) v[q] = nv[q];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) low |= __shfl_xor_sync(FULL, low, o);
+        if (lane_id() == 0 && low) {
+            atomicOr(&sm.hub_bm[0], (unsigned)low);
+            atomicOr(&sm.hub_bm[1], (unsigned)(low >> 32));
         }
         __syncthreads();
         for (int i = threadIdx.x; i < HUB_WORDS; i += BLOCK)
@@ -924,9 +941,10 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
     if (threadIdx.x == 0) sm.out_cnt = 0;
     __syncthreads();
     constexpr unsigned NG = 32 / G;
+    unsigned seg = lo < hi ? list_segment(rc.L[bin], sm.prefix[bin], lo) : 0u;  // once per chunk
     for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG)
         group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out, out_od,
-                                          &sm.out_cnt, sm.win_bm[warp], my_conf, my_edges);
+                                          &sm.out_cnt, sm.win_bm[warp], seg, my_conf, my_edges);
     __syncthreads();
     if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, c, sm.out_cnt);
 }
