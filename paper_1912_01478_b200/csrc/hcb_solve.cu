@@ -544,10 +544,11 @@ __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
 // Warp-level mex over window(s) above color 64, for a node whose colors
 // 1..64 are all taken (rare): whole warp, one node.
 template <class F>
-__device__ unsigned warp_mex_above64(const Params &P, int u, long long b, long long e, unsigned *bm) {
+__device__ unsigned warp_mex_above64(const Params &P, int u, long long b, long long e, unsigned *bm,
+                                     unsigned start) {
     const unsigned lane = lane_id();
     const unsigned lim = (unsigned)(e - b) + 1u;
-    for (unsigned w0 = 64;; w0 += WIN_WORDS * 32) {
+    for (unsigned w0 = start;; w0 += WIN_WORDS * 32) {
         bm[lane] = 0u;
         __syncwarp();
         const unsigned hi = min(lim, w0 + WIN_WORDS * 32);
@@ -595,7 +596,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     const long long e = u >= 0 ? b + (long long)(od & 0xffffull) : 0;
     unsigned iters = (unsigned)((e - b + 4 * G - 1) / (4 * G));
     iters = __reduce_max_sync(FULL, iters);
-    unsigned long long mask = 0;
+    unsigned long long mask = 0, mask2 = 0;  // colors 1..64, 65..128 (mask2: G == 32 only)
     unsigned cnt = 0, low = 0;
     bool stop = u < 0;
     // software pipeline: the column ids of iteration it+1 are in flight while
@@ -621,6 +622,13 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             for (int q = 0; q < 4; ++q) x[q] = nb[q] >= 0 ? xget<F>(P, nb[q]) : 0u;
 #pragma unroll
             for (int q = 0; q < 4; ++q) mask_add<F>(mask, x[q]);
+            if constexpr (G == 32) {  // warp per node: colors 65..128 too (hub-core nodes)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const unsigned c = x[q] & CM<F>;
+                    if ((x[q] & FB<F>) && c > 64u && c <= 128u) mask2 |= 1ull << (c - 65u);
+                }
+            }
         } else {
             unsigned x[4];
 #pragma unroll
@@ -648,15 +656,21 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     if (PHASE == 0) {
 #pragma unroll
         for (int o = G / 2; o > 0; o >>= 1) mask |= __shfl_xor_sync(FULL, mask, o);
+        if constexpr (G == 32) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mask2 |= __shfl_xor_sync(FULL, mask2, o);
+        }
         unsigned T;
         if (mask != ~0ull) {
             T = (unsigned)__ffsll((long long)~mask);
+        } else if (G == 32 && mask2 != ~0ull) {
+            T = 64u + (unsigned)__ffsll((long long)~mask2);  // no second pass over the adjacency
         } else if (G < 32) {
             T = 65u;  // deg <= 64 and colors 1..64 all taken: exactly 64 neighbours
         } else {
             T = 0u;   // warp-uniform (one node per warp): fall back to bitmap windows
         }
-        if (G == 32 && T == 0u && u >= 0) T = warp_mex_above64<F>(P, u, b, e, bm);
+        if (G == 32 && T == 0u && u >= 0) T = warp_mex_above64<F>(P, u, b, e, bm, 128u);
         if (sub == 0 && u >= 0) {
             xput<F>(P, u, T);
             if (STATS) my_edges[0] += e - b;
@@ -702,7 +716,7 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
         // colors w0+1 .. w0+64 (the common ones) go to a register mask,
         // OR-reduced per warp: one shared atomic per warp instead of one per
         // neighbour on the same few hot words
-        unsigned long long low = 0;
+        unsigned long long low = 0, low2 = 0;
         for (long long k = b + threadIdx.x; k < e; k += HU * BLOCK) {
             int nv[HU];
 #pragma unroll
@@ -718,16 +732,26 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
                 const unsigned c = x[q] & CM<F>;
                 if (!(x[q] & FB<F>) || c <= w0 || c > hi) continue;
                 if (c <= w0 + 64u) low |= 1ull << (c - w0 - 1u);
+                else if (c <= w0 + 128u) low2 |= 1ull << (c - w0 - 65u);
                 else mark(sm.hub_bm, c - w0);
             }
 #pragma unroll
             for (int q = 0; q < HU; ++q) v[q] = nv[q];
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) low |= __shfl_xor_sync(FULL, low, o);
-        if (lane_id() == 0 && low) {
-            atomicOr(&sm.hub_bm[0], (unsigned)low);
-            atomicOr(&sm.hub_bm[1], (unsigned)(low >> 32));
+        for (int o = 16; o > 0; o >>= 1) {
+            low |= __shfl_xor_sync(FULL, low, o);
+            low2 |= __shfl_xor_sync(FULL, low2, o);
+        }
+        if (lane_id() == 0) {
+            if (low) {
+                atomicOr(&sm.hub_bm[0], (unsigned)low);
+                atomicOr(&sm.hub_bm[1], (unsigned)(low >> 32));
+            }
+            if (low2) {
+                atomicOr(&sm.hub_bm[2], (unsigned)low2);
+                atomicOr(&sm.hub_bm[3], (unsigned)(low2 >> 32));
+            }
         }
         __syncthreads();
         for (int i = threadIdx.x; i < HUB_WORDS; i += BLOCK)
