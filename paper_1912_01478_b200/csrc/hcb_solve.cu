@@ -833,10 +833,10 @@ struct TileA {
 template <typename OffT, class F, int NP, int PHASE>
 __device__ __forceinline__ void tile_issue(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
-                                           unsigned long long hi, TileA<OffT, NP> &a) {
+                                           unsigned long long hi, TileA<OffT, NP> &a, unsigned &seg) {
+    // seg: segment-walk hint carried across the tiles of a chunk (positions grow)
     const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
-    unsigned seg = ident ? 0u : list_segment(L, prefix, base);  // same for the whole CTA (broadcast)
     // bin-0-only graphs (grids, meshes) read the row offsets: their lists are
     // nearly id-ordered, so the offsets are almost contiguous, and a 4-byte
     // list entry beats the 12-byte (id, od) pair (grid4096 data 843 vs 969 ms)
@@ -1128,9 +1128,10 @@ template <typename OffT, class F, bool STATS, int PHASE>
 __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
                                            unsigned long long hi, TileA<OffT, F::small ? NPT_SMALL : NPT> &a,
-                                           bool *lost, unsigned long long &my_conf, unsigned long long *my_edges) {
+                                           bool *lost, unsigned long long &my_conf, unsigned long long *my_edges,
+                                           unsigned &seg) {
     constexpr int NP = F::small ? NPT_SMALL : NPT;
-    tile_issue<OffT, F, NP, PHASE>(P, ro, rc, prefix, base, hi, a);
+    tile_issue<OffT, F, NP, PHASE>(P, ro, rc, prefix, base, hi, a, seg);
     tile_finish<OffT, F, STATS, PHASE, NP>(P, rc, a, lost, my_conf, my_edges);
 }
 
@@ -1151,10 +1152,12 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     // affects locality, but an unordered list fragments round after round.)
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
     unsigned written = 0, buf = 0;
+    // one segment search per chunk, then walks (not one search per tile)
+    unsigned seg = (rc.ident || lo >= hi) ? 0u : list_segment(rc.L[0], sm.prefix[0], lo);
     for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NP) {
         TileA<OffT, NP> cur;
         bool lost[NP];
-        small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, cur, lost, my_conf, my_edges);
+        small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, cur, lost, my_conf, my_edges, seg);
         const int *u = cur.u;
         if (PHASE == 1) {
             unsigned bal[NP];
@@ -1870,9 +1873,17 @@ static cudaError_t launch_persistent(const void *fn, unsigned nblocks, void **ar
     }
     // only when the whole array fits the set-aside (a partial window measured
     // slower: RMAT-26's 134 MB of words 1533 -> 1547 ms; grid4096 604 -> 590)
-    if (HC_L2_PERSIST && persist_max > 0 && xbytes > 0 && xbytes <= persist_max) {
+    // small arrays stay in L2 anyway; there the window only adds driver calls
+    // (RMAT-16: 2.9 -> 3.9 ms per solve)
+    static size_t limit_set = 0;
+    if (HC_L2_PERSIST && persist_max > 0 && xbytes >= ((size_t)16 << 20) && xbytes <= persist_max) {
         const size_t want = xbytes;
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+        cudaError_t e = cudaSuccess;
+        if (limit_set != want) {  // exactly the array (a larger set-aside slowed the grid 590 -> 605 ms)
+            e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            if (e == cudaSuccess) limit_set = want;
+        }
+        if (e == cudaSuccess) {
             attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
             attr[na].val.accessPolicyWindow.base_ptr = x;
             attr[na].val.accessPolicyWindow.num_bytes = xbytes;
@@ -2015,7 +2026,7 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
         HC_CUDA_TRY(cudaStreamSynchronize(st));
         // the persisting lines go back to normal: nothing of this solve stays
         // pinned in L2 for the caller's next kernel (or the next solve)
-        if (HC_L2_PERSIST) cudaCtxResetPersistingL2Cache();
+        if (HC_L2_PERSIST && (size_t)num_nodes * (x16 ? 2 : 4) >= ((size_t)16 << 20)) cudaCtxResetPersistingL2Cache();
         const unsigned overflow = (unsigned)(info[2] & 0xffffffffLL);
         if (!(x16 && overflow) || x16_exact) break;
         x16 = false;  // redo with 32-bit state words
