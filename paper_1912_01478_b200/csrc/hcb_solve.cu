@@ -89,6 +89,9 @@ constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 #ifndef HC_MG_PLAIN_BARRIER
 #define HC_MG_PLAIN_BARRIER 0
 #endif
+#ifndef HC_PAIR
+#define HC_PAIR 2   // bin-0-only kernel: tiles per loser-compaction barrier
+#endif
 #ifndef HC_NPT_SMALL
 #define HC_NPT_SMALL 2
 #endif
@@ -237,7 +240,7 @@ struct SmemT {
     unsigned win_bm[SMALL ? 1 : NW][WIN_WORDS];
     unsigned hub_bm[SMALL ? 1 : HUB_WORDS];
     unsigned warp_tmp[NPT * NW];
-    unsigned cnt_tab[2][NPT * NW];
+    unsigned cnt_tab[2][2 * NPT * NW];
     unsigned long long red;
     int hub_first;
     unsigned unit;
@@ -1154,26 +1157,47 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     unsigned written = 0, buf = 0;
     // one segment search per chunk, then walks (not one search per tile)
     unsigned seg = (rc.ident || lo >= hi) ? 0u : list_segment(rc.L[0], sm.prefix[0], lo);
-    for (unsigned long long base = lo; base < hi; base += (unsigned long long)BLOCK * NP) {
-        TileA<OffT, NP> cur;
-        bool lost[NP];
-        small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base, hi, cur, lost, my_conf, my_edges, seg);
-        const int *u = cur.u;
-        if (PHASE == 1) {
-            unsigned bal[NP];
+    // the bin-0-only kernel compacts PAIR tiles per barrier
+    constexpr int PAIR = F::small ? HC_PAIR : 1;
+    constexpr int NS = PAIR * NP;  // slices per compaction
+    constexpr unsigned long long STEP = (unsigned long long)BLOCK * NP;
+    for (unsigned long long base = lo; base < hi; base += STEP * PAIR) {
+        int u[NS];
+        bool lost[NS];
+        unsigned long long odv[F::small ? 1 : NS];  // (offset, degree) of the losers (general kernel)
 #pragma unroll
-            for (int j = 0; j < NP; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
-            if (lane < NP) {
+        for (int t = 0; t < PAIR; ++t) {
+            TileA<OffT, NP> cur;
+            bool lt[NP];
+            if (t == 0 || base + t * STEP < hi) {  // CTA-uniform
+                small_tile<OffT, F, STATS, PHASE>(P, ro, rc, sm.prefix[0], base + t * STEP, hi, cur, lt, my_conf,
+                                                  my_edges, seg);
+            } else {
+#pragma unroll
+                for (int q = 0; q < NP; ++q) { cur.u[q] = -1; lt[q] = false; }
+            }
+#pragma unroll
+            for (int q = 0; q < NP; ++q) {
+                u[t * NP + q] = cur.u[q];
+                lost[t * NP + q] = lt[q];
+                if constexpr (!F::small) odv[t * NP + q] = make_od(cur.rb[q], cur.re[q]);
+            }
+        }
+        if (PHASE == 1) {
+            unsigned bal[NS];
+#pragma unroll
+            for (int j = 0; j < NS; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
+            if (lane < NS) {
                 unsigned mine = 0;
 #pragma unroll
-                for (int j = 0; j < NP; ++j)
+                for (int j = 0; j < NS; ++j)
                     if (lane == (unsigned)j) mine = __popc(bal[j]);
                 sm.cnt_tab[buf][lane * NW + warp] = mine;
             }
             __syncthreads();
             unsigned run = written;
 #pragma unroll
-            for (int j = 0; j < NP; ++j) {
+            for (int j = 0; j < NS; ++j) {
                 const unsigned v = lane < NW ? sm.cnt_tab[buf][j * NW + lane] : 0u;
                 const unsigned incl = warp_incl_scan(v);
                 const unsigned before = __shfl_sync(FULL, incl - v, warp);  // warps < me in slice j
@@ -1181,7 +1205,7 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
                 if (lost[j]) {
                     const unsigned pos = run + before + __popc(bal[j] & lanemask_lt());
                     out[pos] = u[j];
-                    if constexpr (!F::small) out_od[pos] = make_od(cur.rb[j], cur.re[j]);
+                    if constexpr (!F::small) out_od[pos] = odv[j];
                 }
                 run += tot_j;
             }
