@@ -1199,9 +1199,8 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
 #pragma unroll
             for (int j = 0; j < NS; ++j) {
                 const unsigned v = lane < NW ? sm.cnt_tab[buf][j * NW + lane] : 0u;
-                const unsigned incl = warp_incl_scan(v);
-                const unsigned before = __shfl_sync(FULL, incl - v, warp);  // warps < me in slice j
-                const unsigned tot_j = __shfl_sync(FULL, incl, 31);
+                const unsigned before = __reduce_add_sync(FULL, lane < warp ? v : 0u);  // warps < me in slice j
+                const unsigned tot_j = __reduce_add_sync(FULL, v);
                 if (lost[j]) {
                     const unsigned pos = run + before + __popc(bal[j] & lanemask_lt());
                     out[pos] = u[j];
