@@ -1,3 +1,6 @@
-from .cli import entrypoint
+"""python -m paper_1912_01478_b200 -> the CLI (cli.py)."""
+import sys
 
-entrypoint()
+from .cli import main
+
+sys.exit(main())
