@@ -611,6 +611,22 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
         const long long k = b + sub + q * G;
         nb[q] = (!stop && k < e) ? colget<F>(P, k, u) : pad;
     }
+    if constexpr (G < 32) {
+        // bins 1 and 2: degree <= 4G, so the first column batch is the whole
+        // adjacency -- one straight pass, no next-batch registers
+        unsigned x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) x[q] = (PHASE == 0 ? nb[q] >= 0 : nb[q] < u) ? xget<F>(P, nb[q]) : 0u;
+        if (PHASE == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mask_add<F>(mask, x[q]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (nb[q] < u) { cnt += (x[q] & CM<F>) == xu; ++low; }
+        }
+        iters = 0;  // the loop below is skipped
+    }
     for (unsigned it = 0; it < iters; ++it) {
         int nx[4];
         const long long kn = b + (long long)(it + 1) * 4 * G + sub;
