@@ -1903,24 +1903,29 @@ static cudaError_t launch_persistent(const void *fn, unsigned nblocks, void **ar
         attr[na].val.cooperative = 1;
         ++na;
     }
-    static size_t persist_max = (size_t)-1;
-    if (persist_max == (size_t)-1) {
-        int dev = 0, v = 0;
-        persist_max = (cudaGetDevice(&dev) == cudaSuccess &&
-                       cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess)
-                          ? (size_t)v : 0;
+    // per-device state (a process may drive several GPUs)
+    constexpr int MAXDEV = 64;
+    static size_t persist_max_of[MAXDEV], limit_set_of[MAXDEV];
+    static bool queried[MAXDEV];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAXDEV) dev = -1;
+    if (dev >= 0 && !queried[dev]) {
+        int v = 0;
+        persist_max_of[dev] =
+            cudaDeviceGetAttribute(&v, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess ? (size_t)v : 0;
+        queried[dev] = true;
     }
+    const size_t persist_max = dev >= 0 ? persist_max_of[dev] : 0;
     // only when the whole array fits the set-aside (a partial window measured
     // slower: RMAT-26's 134 MB of words 1533 -> 1547 ms; grid4096 604 -> 590)
     // small arrays stay in L2 anyway; there the window only adds driver calls
     // (RMAT-16: 2.9 -> 3.9 ms per solve)
-    static size_t limit_set = 0;
     if (HC_L2_PERSIST && persist_max > 0 && xbytes >= ((size_t)16 << 20) && xbytes <= persist_max) {
         const size_t want = xbytes;
         cudaError_t e = cudaSuccess;
-        if (limit_set != want) {  // exactly the array (a larger set-aside slowed the grid 590 -> 605 ms)
+        if (limit_set_of[dev] != want) {  // exactly the array (a larger set-aside slowed the grid 590 -> 605 ms)
             e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-            if (e == cudaSuccess) limit_set = want;
+            if (e == cudaSuccess) limit_set_of[dev] = want;
         }
         if (e == cudaSuccess) {
             attr[na].id = cudaLaunchAttributeAccessPolicyWindow;
