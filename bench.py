@@ -323,9 +323,9 @@ def run_distributed(args, cfg):
     ro_host = dg.row_offsets.cpu().numpy()
     try:
         solver = MgSolver(dg)
-        exchange = ("peer memory: boundary state words stored into every peer's replica by the solve kernel "
-                    "(NVLink), cross-GPU mailbox barriers + (|W|, conflicts) all-reduce; one persistent kernel "
-                    "per GPU")
+        exchange = ("peer memory: one persistent kernel per GPU; boundary state words reach the ranks that read "
+                    "them by NVLink stores (mirrored at write time, or boundary-zone copies per phase, chosen per "
+                    "round); cross-GPU mailbox barriers carry the (|W|, conflicts) all-reduce")
     except Exception as exc:
         solver = None
         exchange = f"NCCL all-gather per phase (peer mapping unavailable: {exc!r})"
