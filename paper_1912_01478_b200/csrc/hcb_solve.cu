@@ -1176,6 +1176,7 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     // the bin-0-only kernel compacts PAIR tiles per barrier
     constexpr int PAIR = F::small ? HC_PAIR : 1;
     constexpr int NS = PAIR * NP;  // slices per compaction
+    static_assert(NS <= 2 * NPT && NS <= 32, "cnt_tab holds 2*NPT slices, one per lane");
     constexpr unsigned long long STEP = (unsigned long long)BLOCK * NP;
     for (unsigned long long base = lo; base < hi; base += STEP * PAIR) {
         int u[NS];
