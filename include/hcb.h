@@ -119,8 +119,10 @@ int hc_wl_swap_and_sort(const int64_t *d_next, const int64_t *d_cursor, int64_t 
 /* Device-resident solve (replaces the color_graph round loop).         */
 /* ------------------------------------------------------------------ */
 
-/* CSR: d_row_offsets int64[n+1], d_col_indices int32[m] (sorted, deduped,
- * symmetric, loop-free as build_csr guarantees).  thr_count = ceil(H*n)
+/* CSR: d_row_offsets int64[n+1], d_col_indices int32[m], symmetric, with each
+ * row's lower-id neighbours first (build_csr's sorted rows qualify; any other
+ * CSR goes through hc_csr_check_lower_first / hc_csr_partition_lower_first,
+ * which the Python layer does for every caller-supplied graph).  thr_count = ceil(H*n)
  * computed by the host exactly as driver.py:138.  Output d_colors int64[n]
  * (0 never appears on success).  d_rec receives up to max_rec round records;
  * *h_rounds = total rounds.  If rounds > max_rec the solve still completes,
@@ -292,6 +294,18 @@ int hc_degree_stats(const int64_t *d_row_offsets, int64_t num_nodes, int64_t *h_
 
 /* int64 -> int32 column conversion for uploads of reference CsrGraph arrays */
 int hc_narrow_i64_i32(const int64_t *d_in, int32_t *d_out, int64_t count, void *stream);
+/* Lower-id-first rows.  hc_solve / hc_mg_solve stop a row's conflict scan at
+ * its first neighbour >= u, so they need each row's lower-id neighbours to be
+ * a prefix of the row (true for build_csr output, graph.py:193-197, which is
+ * sorted).  The reference scans whole rows (_kernels.pyx:106-113), so it
+ * accepts any order; callers with an arbitrary CSR run the check and, when it
+ * reports rows, the stable partition (v < u first) into a second column array.
+ * Colors and every record are row-order independent, so the result is the
+ * reference's.  d_acc: int64[1] device scratch. */
+int hc_csr_check_lower_first(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                             int64_t *d_acc, int64_t *h_bad_rows, void *stream);
+int hc_csr_partition_lower_first(const int64_t *d_row_offsets, const int32_t *d_col_in, int32_t *d_col_out,
+                                 int64_t num_nodes, void *stream);
 
 #ifdef __cplusplus
 }

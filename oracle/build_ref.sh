@@ -18,6 +18,9 @@ rm -rf "$HERE/_ref"
     python -m pip install -q --no-index --no-build-isolation --no-deps \
       --find-links /opt/wheelhouse --target "$HERE/_ref" . )
 rm -rf "$TMP"
+# the reference's own test suite (run against the cuda backend by
+# tests/test_reference_suite.py through tests/refsuite_plugin.py)
+cp -r "$SRC/tests" "$HERE/_ref/tests"
 python - <<PY
 import sys; sys.path.insert(0, "$HERE/_ref")
 import hybridcolor

@@ -5,13 +5,22 @@ The public names mirror the reference package's solve path
 (pkg/src/hybridcolor/__init__.py:11-69): `color_graph`, `HybridConfig`,
 `RunReport`, `RoundRecord`, `colors_used`, `verify_coloring`, `CsrGraph`,
 `EdgeList`, `build_csr`, the per-round `ColorState` / `Worklist` /
-`data_driven_iteration` / `topology_driven_iteration`, and the kernel-module
+`data_driven_iteration` / `topology_driven_iteration` / `assign_color` /
+`resolve_conflicts` / `mex_positive`, and the kernel-module
 registry (`get_kernels`, `available_backends`, `backend_name`).  Everything
 computes on the GPU through libhcb.so (include/hcb.h); there is no CPU path.
 """
 
 from ._backend import available_backends, backend_name, get_kernels
-from .coloring import ColorState, RoundOutcome, data_driven_iteration, topology_driven_iteration
+from .coloring import (
+    ColorState,
+    RoundOutcome,
+    assign_color,
+    data_driven_iteration,
+    mex_positive,
+    resolve_conflicts,
+    topology_driven_iteration,
+)
 from .driver import (
     MODES,
     HybridConfig,
@@ -63,7 +72,8 @@ __version__ = "0.1.0"
 
 __all__ = [
     "available_backends", "backend_name", "get_kernels",
-    "ColorState", "RoundOutcome", "data_driven_iteration", "topology_driven_iteration",
+    "ColorState", "RoundOutcome", "assign_color", "data_driven_iteration", "mex_positive",
+    "resolve_conflicts", "topology_driven_iteration",
     "MODES", "HybridConfig", "RoundRecord", "RunReport", "Solver",
     "color_graph", "colors_used", "threshold_count", "verify_coloring",
     "CsrGraph", "DeviceCsr", "EdgeList", "build_csr", "build_csr_device",

@@ -106,6 +106,8 @@ _SIGS = {
     "hc_verify": (ctypes.c_int, [_p, _p, _i64, _p, _p, _p, _p]),
     "hc_colors_used": (ctypes.c_int, [_p, _i64, _p, _p, _p]),
     "hc_narrow_i64_i32": (ctypes.c_int, [_p, _p, _i64, _p]),
+    "hc_csr_check_lower_first": (ctypes.c_int, [_p, _p, _i64, _p, _p, _p]),
+    "hc_csr_partition_lower_first": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
     "hc_mtx_workspace_bytes": (ctypes.c_size_t, [_i64]),
     "hc_mtx_parse": (ctypes.c_int, [_p, _i64, ctypes.c_int, _i64, _i64, _i64, _p, _p, _p, _p, _p, _p, _p,
                                     ctypes.c_size_t, _p]),

@@ -421,6 +421,58 @@ __global__ void narrow_kernel(const long long *in, int *out, long long count) {
         out[i] = (int)in[i];
 }
 
+
+// ------------------------------------------------------ lower-id-first rows
+// The fused solver's resolve stops scanning a row at its first neighbour >= u
+// (hcb_solve.cu), so it needs every row's lower-id neighbours to form a prefix
+// of the row.  build_csr output (graph.py:193-197: sorted ascending) has that
+// property; an arbitrary caller CSR may not.  The reference resolve scans the
+// whole row (_kernels.pyx:106-113) and every solve output is a function of the
+// row *sets* (mex, the v<u conflict count), so a stable partition of each row
+// into (v < u) then (v >= u) changes nothing but the scan order.
+__global__ void lower_first_check_kernel(const long long *ro, const int *ci, long long n,
+                                         unsigned long long *acc) {
+    const unsigned lane = lane_id();
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long bad = 0;
+    for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
+        bool seen_high = false, violates = false;
+        for (long long k0 = ro[u]; k0 < ro[u + 1] && !violates; k0 += 32) {
+            const long long k = k0 + lane;
+            const bool in = k < ro[u + 1];
+            const long long v = in ? ci[k] : 0;
+            const unsigned high = __ballot_sync(FULL, in && v >= u);
+            const unsigned low = __ballot_sync(FULL, in && v < u);
+            if (seen_high && low) violates = true;
+            // a low after the first high inside this chunk
+            if (high && (low >> (__ffs(high) - 1)) != 0u) violates = true;
+            seen_high |= high != 0u;
+        }
+        bad += (violates && lane == 0);
+    }
+    bad = warp_sum(bad);
+    if (lane == 0 && bad) atomicAdd(acc, bad);
+}
+
+__global__ void lower_first_partition_kernel(const long long *ro, const int *in, int *out, long long n) {
+    const unsigned lane = lane_id();
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nwarps) {
+        const long long b = ro[u], e = ro[u + 1];
+        long long w = b;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (long long k0 = b; k0 < e; k0 += 32) {
+                const long long k = k0 + lane;
+                const int v = k < e ? in[k] : 0;
+                const bool take = k < e && ((pass == 0) == ((long long)v < u));
+                const unsigned m = __ballot_sync(FULL, take);
+                if (take) out[w + __popc(m & ((1u << lane) - 1u))] = v;
+                w += __popc(m);
+            }
+        }
+    }
+}
+
 struct CsrLayout {
     size_t deg, off, cur, tmp, uniq, ro_u, rows, status, bitmaps, scan, part, total;
     int big_ctas;
@@ -595,6 +647,31 @@ int hc_narrow_i64_i32(const int64_t *d_in, int32_t *d_out, int64_t count, void *
     if (count == 0) return HC_OK;
     narrow_kernel<<<grid_cap(count, BLOCK), BLOCK, 0, as_stream(stream)>>>((const long long *)d_in,
                                                                            d_out, count);
+    HC_CHECK_LAUNCH();
+    return HC_OK;
+}
+
+int hc_csr_check_lower_first(const int64_t *d_ro, const int32_t *d_ci, int64_t n, int64_t *d_acc,
+                             int64_t *h_bad_rows, void *stream) {
+    HC_REQUIRE(n >= 0 && d_acc && h_bad_rows, HC_ERR_INVALID, "check_lower_first: bad arguments");
+    cudaStream_t st = as_stream(stream);
+    HC_CUDA_TRY(cudaMemsetAsync(d_acc, 0, sizeof(int64_t), st));
+    if (n > 0) {
+        lower_first_check_kernel<<<grid_cap(n, BLOCK / 32), BLOCK, 0, st>>>(
+            (const long long *)d_ro, d_ci, n, (unsigned long long *)d_acc);
+        HC_CHECK_LAUNCH();
+    }
+    HC_CUDA_TRY(cudaMemcpyAsync(h_bad_rows, d_acc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    return HC_OK;
+}
+
+int hc_csr_partition_lower_first(const int64_t *d_ro, const int32_t *d_ci_in, int32_t *d_ci_out, int64_t n,
+                                 void *stream) {
+    HC_REQUIRE(n >= 0 && d_ci_in != d_ci_out, HC_ERR_INVALID, "partition_lower_first: bad arguments");
+    if (n == 0) return HC_OK;
+    lower_first_partition_kernel<<<grid_cap(n, BLOCK / 32), BLOCK, 0, as_stream(stream)>>>(
+        (const long long *)d_ro, d_ci_in, d_ci_out, n);
     HC_CHECK_LAUNCH();
     return HC_OK;
 }

@@ -143,7 +143,7 @@ class Solver:
 
     def __init__(self, graph: DeviceCsr, max_rec: int | None = None):
         self.L = _lib.load()
-        self.g = graph
+        self.g = graph.ensure_lower_first()
         dev = graph.device
         n = graph.num_nodes
         self.ws = _lib.workspace(self.L.hc_solve_workspace_bytes(n, graph.num_edges), dev)
@@ -230,7 +230,9 @@ def color_graph(
     if n == 0:  # driver.py:145 never enters the loop
         report.valid = True
         return np.zeros(0, dtype=np.int64), report
-    solver = Solver(dg)
+    solver = dg.__dict__.get("_solver")
+    if solver is None:  # one workspace per graph, reused by later calls (benchmarks)
+        solver = dg.__dict__["_solver"] = Solver(dg)
     res = solver.run(config.mode, threshold_count(config, n))
     report.total_seconds = res.seconds
     for r in res.records:

@@ -78,6 +78,12 @@ class CsrGraph:
     def neighbors(self, u: int) -> np.ndarray:
         return self.col_indices[self.row_offsets[u] : self.row_offsets[u + 1]]
 
+    def to_edge_list(self) -> EdgeList:
+        """One (u, v) pair per undirected edge, u < v side (graph.py:86-93)."""
+        src = np.repeat(np.arange(self.num_nodes, dtype=ID_DTYPE), self.degrees)
+        keep = src < self.col_indices
+        return EdgeList(self.num_nodes, np.column_stack((src[keep], self.col_indices[keep])))
+
     @classmethod
     def pinned(cls, g: "CsrGraph") -> "CsrGraph":
         """Copy of `g` whose arrays live in page-locked host memory, so uploads
@@ -86,6 +92,7 @@ class CsrGraph:
         ci = torch.from_numpy(np.array(g.col_indices)).pin_memory()
         out = cls(g.num_nodes, g.num_edges, ro.numpy(), ci.numpy())
         out._pinned = (ro, ci)
+        out._lower_first = getattr(g, "_lower_first", None)
         return out
 
     def _host_tensors(self):
@@ -108,7 +115,7 @@ class CsrGraph:
             _lib.check(_lib.load().hc_narrow_i64_i32(ci64.data_ptr(), ci32.data_ptr(), m,
                                                       _lib.stream_handle()))
             del ci64
-        return DeviceCsr(n, m, ro, ci32, host=self)
+        return DeviceCsr(n, m, ro, ci32, host=self, lower_first=getattr(self, "_lower_first", None))
 
 
 @dataclass
@@ -121,6 +128,34 @@ class DeviceCsr:
     col_indices: torch.Tensor
     host: CsrGraph | None = field(default=None, repr=False)
     _ci64: torch.Tensor | None = field(default=None, repr=False)
+    # True when every row lists its lower-id neighbours first (build_csr output
+    # is sorted, graph.py:193-197); None = unknown (caller-supplied CSR), checked
+    # on the device by ensure_lower_first() before a solve.
+    lower_first: bool | None = field(default=None, repr=False)
+
+    def ensure_lower_first(self) -> "DeviceCsr":
+        """Make each row's lower-id neighbours a prefix of the row (the fused
+        solve's early-exit precondition, include/hcb.h).  A caller CSR with
+        unsorted rows gets a stable-partitioned copy of its columns on the
+        device; solve outputs depend only on the row sets, so the result is
+        the reference's (which scans whole rows, _kernels.pyx:106-113)."""
+        if self.lower_first or self.num_edges == 0:
+            self.lower_first = True
+            return self
+        L = _lib.load()
+        acc = torch.zeros(1, dtype=torch.int64, device=self.device)
+        bad = ctypes.c_int64(0)
+        _lib.check(L.hc_csr_check_lower_first(self.row_offsets.data_ptr(), _lib.ptr(self.col_indices),
+                                              self.num_nodes, acc.data_ptr(), ctypes.byref(bad),
+                                              _lib.stream_handle()))
+        if bad.value:
+            out = torch.empty_like(self.col_indices)
+            _lib.check(L.hc_csr_partition_lower_first(self.row_offsets.data_ptr(), _lib.ptr(self.col_indices),
+                                                      _lib.ptr(out), self.num_nodes, _lib.stream_handle()))
+            self.col_indices = out
+            self._ci64 = None
+        self.lower_first = True
+        return self
 
     @property
     def num_undirected_edges(self) -> int:
@@ -156,6 +191,8 @@ class DeviceCsr:
             self.host = CsrGraph(self.num_nodes, self.num_edges,
                                  self.row_offsets.cpu().numpy(),
                                  self.col_indices.cpu().numpy().astype(np.int64))
+            if self.lower_first:
+                self.host._lower_first = True
         return self.host
 
 
@@ -179,7 +216,7 @@ def build_csr_device(d_edges: torch.Tensor, num_nodes: int) -> DeviceCsr:
     del ws
     md = int(mdir.value)
     ci = ci[:md].clone() if md else ci[:0]
-    return DeviceCsr(n, md, ro, ci)
+    return DeviceCsr(n, md, ro, ci, lower_first=True)  # rows sorted ascending
 
 
 def build_csr(edge_list: EdgeList) -> CsrGraph:

@@ -104,3 +104,40 @@ def grid_closed_form(rows: int, cols: int):
     """Checkerboard colors 1+((i+j) mod 2), rounds ceil((r+c)/2)."""
     i, j = np.meshgrid(np.arange(rows), np.arange(cols), indexing="ij")
     return (1 + ((i + j) % 2)).ravel().astype(np.int64), -(-(rows + cols) // 2)
+
+
+def grid_records(rows: int, cols: int, mode: str = "hybrid", threshold_fraction: float = 0.6) -> np.ndarray:
+    """Closed form of every per-round record (topo?, wl_in, wl_out, conflicts)
+    of color_graph on the rows x cols 4-neighbour grid (ids i*cols+j).
+
+    Lower-id neighbours of (i,j) are (i-1,j) and (i,j-1), both on antidiagonal
+    d-1 (d = i+j).  Round 1 everyone takes color 1 and only node 0 wins.  In
+    round t >= 2 antidiagonal 2t-3 (its lower neighbours committed with color 1)
+    takes 2 and wins, antidiagonal 2t-2 takes 1 and wins (its lower neighbours
+    hold 2), every later antidiagonal takes 1 and loses to its lower
+    neighbours.  So after round t antidiagonals 0..2t-2 are final:
+      wl_out(t) = n - F(2t-2),  wl_in(t) = wl_out(t-1) (wl_in(1) = n),
+      conflicts(t) = m_und - S(2t-2),
+    F(k) / S(k) = nodes / lower-neighbour edges on antidiagonals <= k.  The mode
+    is driver.py:147-152 with thr = ceil(H*n) (driver.py:138).  Pinned against
+    the reference's own records (tests/golden/grids.npz, make_grid_golden.py)."""
+    import math
+
+    n = rows * cols
+    if n == 0:
+        return np.zeros((0, 4), np.int64)
+    d = np.arange(rows + cols - 1, dtype=np.int64)
+    cnt = np.minimum(d, rows - 1) - np.maximum(0, d - cols + 1) + 1
+    low = 2 * cnt - (d <= cols - 1) - (d <= rows - 1)  # i>0 nodes + j>0 nodes
+    F = np.concatenate(([0], np.cumsum(cnt)))            # F[k+1] = nodes on diagonals <= k
+    S = np.concatenate(([0], np.cumsum(low)))
+    m_und = int(S[-1])
+    R = -(-(rows + cols) // 2)
+    thr = math.ceil(threshold_fraction * n)
+    out = np.zeros((R, 4), np.int64)
+    for t in range(1, R + 1):
+        k_out = min(2 * t - 2, rows + cols - 2)
+        wl_in = n if t == 1 else n - int(F[min(2 * t - 4, rows + cols - 2) + 1])
+        topo = mode == "topo" or (mode == "hybrid" and wl_in > thr)
+        out[t - 1] = (int(topo), wl_in, n - int(F[k_out + 1]), m_und - int(S[k_out + 1]))
+    return out

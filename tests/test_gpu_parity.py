@@ -5,7 +5,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import CONFIG_SPECS, MODES, THRESHOLDS, csr_sha, grid_closed_form
+from conftest import CONFIG_SPECS, MODES, THRESHOLDS, csr_sha, grid_closed_form, grid_records
 from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
@@ -108,6 +108,29 @@ def test_grid_closed_form(rows, cols):
     colors, rep = hc.color_graph(dg)
     assert np.array_equal(colors, want) and rep.total_rounds == rounds
     assert rep.per_round[0].conflicts == G.grid_num_pairs(rows, cols)
+
+
+def test_headline_grid4096_every_round_every_mode():
+    """configs[1] at full size: colors and all 4096 per-round records in data,
+    topo and hybrid mode equal the reference-pinned closed form
+    (conftest.grid_records; pinned by test_oracle.py::
+    test_grid_record_closed_form_vs_reference)."""
+    dg = G.grid_graph(4096, 4096)
+    want, rounds = grid_closed_form(4096, 4096)
+    for mode in MODES:
+        colors, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+        assert rep.total_rounds == rounds == 4096
+        assert np.array_equal(_recs(rep), grid_records(4096, 4096, mode, 0.6)), mode
+        assert np.array_equal(colors, want), mode
+        assert rep.valid and rep.colors_used == 2
+
+
+@pytest.mark.parametrize("rows,cols", [(1000, 37), (3, 2000), (777, 1500)])
+def test_grid_records_closed_form(rows, cols):
+    dg = G.grid_graph(rows, cols)
+    for mode, thr in (("hybrid", 0.6), ("hybrid", 0.2), ("data", 0.6), ("topo", 0.6)):
+        _, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode, threshold_fraction=thr))
+        assert np.array_equal(_recs(rep), grid_records(rows, cols, mode, thr)), (mode, thr)
 
 
 @pytest.mark.parametrize("scale,seed", [(12, 1), (14, 3)])
@@ -275,3 +298,55 @@ def test_forced_storage_formats_vs_golden(configs, fmt):
     finally:
         L.hc_solve_set_formats(0, 0, 0)
         L.hc_solve_set_small(1)
+
+
+# ---------------------------------------------------------------- unsorted caller CSR
+def _shuffle_rows(ro, ci, rng):
+    ci = ci.copy()
+    for u in range(len(ro) - 1):
+        rng.shuffle(ci[ro[u]:ro[u + 1]])
+    return ci
+
+
+def test_unsorted_rows_match_reference(corpus):
+    """A caller CSR whose rows are not sorted (a user-built CsrGraph, a
+    third-party .npz): the reference scans whole rows (_kernels.pyx:106-113) so
+    its result does not depend on row order; the device path partitions such
+    rows (lower ids first, hc_csr_partition_lower_first) and must give the
+    reference's colors and records."""
+    rng = np.random.default_rng(7)
+    done = 0
+    for g in corpus[::5]:
+        if g.n == 0 or len(g.ci) == 0:
+            continue
+        ci = _shuffle_rows(g.ro, g.ci, rng)
+        for mode in MODES:
+            colors, rep = hc.color_graph(hc.CsrGraph(g.n, len(ci), g.ro, ci), hc.HybridConfig(mode=mode))
+            assert np.array_equal(colors, g.colors), (g.name, mode)
+            assert np.array_equal(_recs(rep), g.records[(mode, 0.6)]), (g.name, mode)
+        done += 1
+    assert done > 40
+    # hubs and the larger bins
+    e = O.gen_rmat(14, 16, 5)
+    ro, ci = O.build_csr(1 << 14, e)
+    want, rec = O.color(ro, ci, "hybrid")
+    shuffled = _shuffle_rows(ro, ci, rng)
+    dg = hc.CsrGraph(1 << 14, len(ci), ro, shuffled).to_device()
+    assert dg.lower_first is None
+    colors, rep = hc.color_graph(dg)
+    assert np.array_equal(colors, want) and np.array_equal(_recs(rep), rec)
+    part = dg.col_indices.cpu().numpy()
+    for u in range(0, 1 << 14, 97):
+        row = part[ro[u]:ro[u + 1]]
+        low = row < u
+        k = int(low.sum())
+        assert low[:k].all() and not low[k:].any(), u                      # lower ids form a prefix
+        assert np.array_equal(np.sort(row), ci[ro[u]:ro[u + 1]]), u          # same multiset
+
+
+def test_sorted_caller_csr_is_not_copied():
+    ro, ci = O.build_csr(500, O.gen_er(500, 3000, 3))
+    dg = hc.CsrGraph(500, len(ci), ro, ci).to_device()
+    before = dg.col_indices.data_ptr()
+    dg.ensure_lower_first()
+    assert dg.lower_first and dg.col_indices.data_ptr() == before

@@ -4,7 +4,7 @@ outputs recorded in tests/golden (and the reference's known answers)."""
 import numpy as np
 import pytest
 
-from conftest import CONFIG_SPECS, MODES, THRESHOLDS, csr_sha, grid_closed_form
+from conftest import CONFIG_SPECS, GOLDEN, MODES, THRESHOLDS, csr_sha, grid_closed_form, grid_records
 from oracle import oracle as O
 
 
@@ -76,3 +76,38 @@ def test_grid_closed_form(rows, cols):
     want, rounds = grid_closed_form(rows, cols)
     assert np.array_equal(colors, want) and rec.shape[0] == rounds
     assert rec[0, 3] == O.grid_num_edges(rows, cols)  # round-1 conflicts = #undirected edges
+
+
+def test_grid_record_closed_form_vs_reference():
+    """The per-round closed form (conftest.grid_records) equals the REFERENCE's
+    records (tests/golden/grids.npz, make_grid_golden.py: the reference's
+    color_graph on its own grid builder) on every shape up to 512^2 and on
+    rectangles, in every mode and threshold recorded; the colors are the
+    checkerboard."""
+    import hashlib
+
+    z = np.load(GOLDEN / "grids.npz")
+    checked = 0
+    for r, c in z["shapes"].tolist():
+        want_colors, rounds = grid_closed_form(r, c)
+        sha = hashlib.sha256(want_colors.astype("<i8").tobytes()).hexdigest()
+        for setting in z["settings"].tolist():
+            mode, thr = setting.split(":")
+            key = f"{r}x{c}__{mode}__{thr}"
+            ref = z[key + "__rec"]
+            assert np.array_equal(grid_records(r, c, mode, float(thr)), ref), key
+            assert ref.shape[0] == rounds and str(z[key + "__colors_sha"]) == sha, key
+            checked += 1
+    assert checked == 20 * 6
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_grid_record_closed_form_vs_oracle(seed):
+    rng = np.random.default_rng(seed)
+    for _ in range(12):
+        r, c = (int(x) for x in rng.integers(1, 90, 2))
+        ro, ci = O.build_csr(r * c, O.gen_grid(r, c))
+        for mode in MODES:
+            thr = float(rng.choice(THRESHOLDS))
+            _, rec = O.color(ro, ci, mode, thr)
+            assert np.array_equal(rec, grid_records(r, c, mode, thr)), (r, c, mode, thr)
