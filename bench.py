@@ -59,44 +59,76 @@ def peaks():
 
 
 # --------------------------------------------------------------------------
-# algorithmic byte model: per round t, W = processed nodes,
-# E = sum of their degrees, El = lower-id neighbours scanned by resolve
-#   assign : data 16|W| + 8E          topo 4n_sweep + 12|W| + 8E
-#   resolve: data 20|W| + 8El         topo 4n_sweep + 16|W| + 8El
-# (4 B list entry, 8 B row offset, 4 B X write / X read / push, 4+4 B per edge)
+# algorithmic byte models.  Per round t: W = processed nodes (wl_in), E = sum
+# of their degrees, El = their lower-id neighbours (hc_solve_stats), W' =
+# wl_out; n nodes, m directed half-edges.
+#
+# SURVEY.md §8(d) (the roofline.achieved numerator; scan-based assign, int32
+# ids/colors, int64 offsets, int64 packed (t,T)):
+#   assign : data 20|W| + 8E         topo 4n + 16|W| + 8E
+#   resolve: data 24|W| + 12El + 4|W'|   topo 4n + 20|W| + 12El + 4|W'|
+#
+# the implemented algorithm (bitmap assign, one 4 B state word,
+# 4 B ids): assign reads the list entry and the node's forbidden-color word and
+# writes the tentative word; resolve reads list, offsets, own word and per lower
+# neighbour (column + word), writes the word or the push; every winner adds
+# its color to each neighbour's bitmap once per solve (column + RED word):
+#   assign : data 12|W|              topo 4n + 8|W|
+#   resolve: data 20|W| + 8El        topo 4n + 16|W| + 8El
+#   + 8m per solve
 # --------------------------------------------------------------------------
-def algorithmic_bytes(records: np.ndarray, stats: np.ndarray, n: int) -> int:
+def survey_bytes(records: np.ndarray, stats: np.ndarray, n: int) -> int:
     total = 0
     for r, (ea, er) in zip(records, stats):
+        topo, w, w2 = int(r[1]), int(r[2]), int(r[3])
+        if topo:
+            total += 4 * n + 16 * w + 8 * int(ea) + 4 * n + 20 * w + 12 * int(er) + 4 * w2
+        else:
+            total += 20 * w + 8 * int(ea) + 24 * w + 12 * int(er) + 4 * w2
+    return total
+
+
+def own_bytes(records: np.ndarray, stats: np.ndarray, n: int, m: int) -> int:
+    total = 8 * m
+    for r, (_, er) in zip(records, stats):
         topo, w = int(r[1]), int(r[2])
         if topo:
-            total += 4 * n + 12 * w + 8 * int(ea) + 4 * n + 16 * w + 8 * int(er)
+            total += 4 * n + 8 * w + 4 * n + 16 * w + 8 * int(er)
         else:
-            total += 16 * w + 8 * int(ea) + 20 * w + 8 * int(er)
+            total += 12 * w + 20 * w + 8 * int(er)
     return total
 
 
 def measured_traffic(config):
-    """DRAM bytes (read + write) of one solve_kernel launch of this config from
-    the committed ncu capture (profiles/r01_<config>_traffic.csv, written by
-    scripts/gpu_round.sh: dram__bytes_read.sum + dram__bytes_write.sum,
+    """DRAM bytes (read + write), duration and L2 hit rate of one solve_kernel
+    launch of this config from the committed ncu capture of the current code
+    (profiles/r02_<config>_traffic.csv, scripts/profile_configs.sh:
+    dram__bytes_read.sum + dram__bytes_write.sum, gpu__time_duration.sum,
     --clock-control none), or None when there is no capture."""
     import csv
 
-    p = REPO / "profiles" / f"r01_{config}_traffic.csv"
+    p = REPO / "profiles" / f"r02_{config}_traffic.csv"
     if not p.exists():
         return None
-    per_launch = {}
+    per = {}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1, "us": 1e3, "ms": 1e6,
+             "s": 1e9, "%": 1}
     with p.open() as f:
         for row in csv.DictReader(ln for ln in f if ln.startswith('"')):
             if "solve_kernel" not in row.get("Kernel Name", ""):
                 continue
-            if row["Metric Name"] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-                key = row["ID"]
-                per_launch[key] = per_launch.get(key, 0) + int(float(row["Metric Value"].replace(",", "")))
-    if not per_launch:
+            d = per.setdefault(row["ID"], {})
+            v = float(row["Metric Value"].replace(",", "")) * scale.get(row.get("Metric Unit", ""), 1)
+            d[row["Metric Name"]] = v
+    rows = [d for d in per.values() if "dram__bytes_read.sum" in d and "dram__bytes_write.sum" in d]
+    if not rows:
         return None
-    return int(sum(per_launch.values()) / len(per_launch))
+    k = len(rows)
+    out = {"bytes": int(sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in rows) / k),
+           "ns": int(sum(d.get("gpu__time_duration.sum", 0) for d in rows) / k)}
+    if all("lts__t_sector_hit_rate.pct" in d for d in rows):
+        out["l2_hit_pct"] = sum(d["lts__t_sector_hit_rate.pct"] for d in rows) / k
+    return out
 
 
 class Clocks:
@@ -290,20 +322,30 @@ def build_graph(hc, cfg):
     return hc.rmat_graph(cfg["scale"], cfg["edgefactor"], cfg["seed"])
 
 
+def gen_edges(hc, cfg):
+    """The config's pair list generated on the current GPU."""
+    from paper_1912_01478_b200 import graph as G
+
+    if cfg["kind"] == "grid":
+        return G.gen_grid_edges(cfg["rows"], cfg["cols"]), cfg["rows"] * cfg["cols"]
+    if cfg["kind"] == "er":
+        return G.gen_er_edges(cfg["n"], cfg["n"] * cfg["avg_degree"] // 2, cfg["seed"]), cfg["n"]
+    return G.gen_rmat_edges(cfg["scale"], cfg["edgefactor"], cfg["seed"]), 1 << cfg["scale"]
+
+
 def run_distributed(args, cfg):
     """N > 1: one rank per GPU, 1D edge-balanced vertex partition of the same
-    graph (strong scaling).  The product path is the device-resident
-    peer-memory solve (multigpu.MgSolver: one persistent kernel per GPU,
-    boundary words stored into the peers' replicas over NVLink, cross-GPU
-    mailbox barriers); if the peer mapping is refused on this box, every rank
-    falls back to the NCCL per-phase exchange (distributed.dist_color_graph)
-    and the line says so."""
+    graph (strong scaling).  Every rank generates the pair list, cuts the same
+    bounds and builds ONLY its own CSR rows (multigpu.build_shard); the solve
+    is the device-resident peer-memory solve (multigpu.MgSolver: one
+    persistent kernel per GPU, boundary words stored into the peers' replicas
+    over NVLink, cross-GPU mailbox barriers).  No fallback: a refused peer
+    mapping is an error."""
     import torch
     import torch.distributed as dist
 
     import paper_1912_01478_b200 as hc
-    from paper_1912_01478_b200.distributed import dist_color_graph
-    from paper_1912_01478_b200.multigpu import MgSolver
+    from paper_1912_01478_b200.multigpu import CsrShard, MgSolver, build_shard, edge_partition_bounds
 
     world = int(os.environ["WORLD_SIZE"])
     rank = int(os.environ.get("RANK", "0"))
@@ -316,31 +358,22 @@ def run_distributed(args, cfg):
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=dev)
-    dg = build_graph(hc, cfg)
-    n, und = dg.num_nodes, dg.num_undirected_edges
+    edges, n = gen_edges(hc, cfg)
+    bounds, raw = edge_partition_bounds(edges, n, world)
+    shard = build_shard(edges, n, bounds, rank, raw)
+    del edges, raw
+    torch.cuda.empty_cache()
+    solver = MgSolver(shard)
+    und = shard.num_undirected_edges
     hcfg = hc.HybridConfig(mode=args.mode)
     thr = hc.threshold_count(hcfg, n)
-    ro_host = dg.row_offsets.cpu().numpy()
-    try:
-        solver = MgSolver(dg)
-        exchange = ("peer memory: one persistent kernel per GPU; boundary state words reach the ranks that read "
-                    "them by NVLink stores (mirrored at write time, or boundary-zone copies per phase, chosen per "
-                    "round); cross-GPU mailbox barriers carry the (|W|, conflicts) all-reduce")
-    except Exception as exc:
-        solver = None
-        exchange = f"NCCL all-gather per phase (peer mapping unavailable: {exc!r})"
-
-    def step(graph=dg, ro=ro_host, slv=None):
-        slv = slv or solver
-        if slv is not None:
-            rounds, _ = slv.run(args.mode, thr)
-            return rounds
-        return dist_color_graph(graph.row_offsets, graph.col_indices, n, hcfg,
-                                host_row_offsets=ro).report.total_rounds
+    exchange = ("peer memory: one persistent kernel per GPU; boundary state words reach the ranks that read "
+                "them by NVLink stores (mirrored at write time, or boundary-zone copies per phase, chosen per "
+                "round); cross-GPU mailbox barriers carry the (|W|, conflicts) all-reduce")
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
-        step()
+        solver.run(args.mode, thr)
     stream = torch.cuda.current_stream()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -351,7 +384,7 @@ def run_distributed(args, cfg):
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed steps, outside the events
             starts[i].record(stream)
-            rounds = step()
+            rounds, _ = solver.run(args.mode, thr)
             stops[i].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
@@ -362,63 +395,61 @@ def run_distributed(args, cfg):
     total_ms = float(t.item())
     value = und * args.steps / (total_ms / 1e3)
 
-    # correctness of the timed path: global coloring valid, same on every rank
-    colors = solver.gather_colors() if solver is not None else None
-    valid = None
-    if colors is not None:
-        valid = hc.verify_coloring(dg, colors) == 0
+    # correctness of the timed path: the global coloring is valid
+    colors = solver.gather_colors()
+    valid = solver.verify(colors) == 0
 
-    # e2e: host CSR (pinned) uploaded by every rank, solve, colors gathered and
-    # copied back, inside the timed region
-    host = hc.CsrGraph.pinned(dg.to_host())
+    # e2e: every rank uploads ITS rows from pinned host memory (one CSR in
+    # total), solves, gathers the colors and copies them back
+    host = shard.to_host()
+    shard_bytes = 8 * host[0].numel() + 8 * host[1].numel()
     e2e_total = 0.0
     for i in range(args.warmup + args.steps):
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
-        d2 = host.to_device(dev)
-        if solver is not None:
-            # the peer mapping is made once (as a long-lived server would);
-            # the freshly uploaded CSR replaces the resident one
-            solver.g = solver.rs.g = d2
-            solver.run(args.mode, thr)
-            solver.gather_colors().cpu()
-        else:
-            dist_color_graph(d2.row_offsets, d2.col_indices, n, hcfg, host_row_offsets=ro_host)
+        solver.replace_shard(CsrShard.upload(host, shard, dev))  # the peer mapping is made once
+        solver.run(args.mode, thr)
+        solver.gather_colors().cpu()
         torch.cuda.synchronize()
         if i >= args.warmup:
             e2e_total += (time.perf_counter() - t0) * 1e3
-        del d2
-    t = torch.tensor([e2e_total], device=cdev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_total = float(t.item())
+    t = torch.tensor([e2e_total, float(shard_bytes), float(shard.nbytes())], device=cdev)
+    tm = t.clone()
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    e2e_total = float(tm[0].item())
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPU",
+            "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPUs (per-rank shards)",
             "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": args.mode,
                        "num_nodes": n, "num_undirected_edges": und, "rounds": rounds,
-                       "parallelism": f"1d-partition x{world} (edge-balanced)", "exchange": exchange,
-                       "valid": valid, "l2": "flushed between timed steps (512 MiB write)"},
+                       "parallelism": f"1d-partition x{world} (edge-balanced, per-rank CSR shards)",
+                       "exchange": exchange, "valid": valid, "bounds": bounds,
+                       "csr_shard_bytes_max": int(tm[2].item()), "csr_bytes_total": int(t[2].item()),
+                       "l2": "flushed between timed steps (512 MiB write)"},
             "clocks": clk.summary(),
-            # peer path: bucket sort (3) + copy_totals + fill_od + narrow + delta + max_degree
-            # + boundary flags + the solve kernel; host-staged path: 4 kernels per round
-            "gpu_launches": (10 if solver is not None else 4 * rounds + 3) * args.steps,
+            # bucket sort (3) + copy_totals + fill_od + narrow + delta + boundary flags + the solve kernel
+            "gpu_launches": 9 * args.steps,
             "e2e": {"value": und * args.steps / (e2e_total / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": world * (8 * (n + 1) + 8 * dg.num_edges),
-                    "d2h_bytes_per_step": world * 8 * n},
+                    "h2d_bytes_per_step": int(t[1].item()), "d2h_bytes_per_step": 8 * n},
             "step_ms": step_ms,
         }
         print(json.dumps(line), flush=True)
-    if solver is not None:
-        solver.close()
+    solver.close()
     dist.destroy_process_group()
     return 0
 
 
-def run_ours(args, cfg):
+def measure(args, name: str, steps: int, warmup: int, *, e2e_steps: int, mode_reps: int,
+            cpu_budget: float) -> dict:
+    """One config on this GPU: the timed hybrid steps, the GPU's own data /
+    topology modes, e2e through color_graph on pinned host buffers, the
+    roofline of the solve under both byte models, and the reference's CPU
+    solve on the host cores (a full solve when it fits cpu_budget)."""
     import ctypes
 
     import torch
@@ -426,22 +457,20 @@ def run_ours(args, cfg):
     import paper_1912_01478_b200 as hc
     from paper_1912_01478_b200 import _lib
 
-    world, rank, local = 1, 0, int(os.environ.get("LOCAL_RANK", "0"))  # N > 1: run_distributed
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-
+    cfg = CONFIGS[name]
+    dev = torch.device("cuda", torch.cuda.current_device())
     dg = build_graph(hc, cfg)
     torch.cuda.synchronize()
-    n, und = dg.num_nodes, dg.num_undirected_edges
+    n, und, m = dg.num_nodes, dg.num_undirected_edges, dg.num_edges
     hcfg = hc.HybridConfig(mode=args.mode)
     thr = hc.threshold_count(hcfg, n)
     solver = hc.Solver(dg)
     L = _lib.load()
 
-    # one instrumented solve (outside the timed region) for the byte model
+    # one instrumented solve (outside the timed region) for the byte models
     stats = torch.zeros((solver.max_rec, 2), dtype=torch.int64, device=dev)
     rounds = ctypes.c_int64(0)
-    _lib.check(L.hc_solve_stats(dg.row_offsets.data_ptr(), _lib.ptr(dg.col_indices), n, dg.num_edges,
+    _lib.check(L.hc_solve_stats(dg.row_offsets.data_ptr(), _lib.ptr(dg.col_indices), n, m,
                                 _lib.MODE_CODES[args.mode], thr, solver.colors.data_ptr(),
                                 solver.rec.data_ptr(), solver.max_rec, ctypes.byref(rounds),
                                 stats.data_ptr(), solver.ws.data_ptr(), solver.ws.numel(),
@@ -449,25 +478,25 @@ def run_ours(args, cfg):
     R = int(rounds.value)
     recs = solver.rec[:R].cpu().numpy()
     st = stats[:R].cpu().numpy()
-    b_alg = algorithmic_bytes(recs, st, n)
-    sum_visits = int(recs[:, 2].sum())
+    b_survey = survey_bytes(recs, st, n)
+    b_own = own_bytes(recs, st, n, m)
 
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         solver.run(args.mode, thr, fetch_records=False)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    stops = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    stops = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     stream = torch.cuda.current_stream()
     # bucket count/scan/scatter + copy_totals + fill_od + narrow_offsets and
-    # delta_columns (int32-offset graphs) + solve_kernel (see the ncu launch list)
-    narrow = dg.num_edges < (1 << 31) - 1
-    launches_per_step = 3 + 1 + 1 + (1 if narrow else 0) + (1 if narrow and dg.num_edges else 0) + 1
+    # delta_columns (int32-offset graphs) + fbx memset + solve_kernel (see the ncu launch list)
+    narrow = m < (1 << 31) - 1
+    launches_per_step = 3 + 1 + 1 + (1 if narrow else 0) + (1 if narrow and m else 0) + 1
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
-        for i in range(args.steps):
+    with Clocks(dev.index) as clk:
+        for i in range(steps):
             flush.zero_()  # L2 flush between timed steps, outside the events
             starts[i].record(stream)
-            rc = L.hc_solve(dg.row_offsets.data_ptr(), _lib.ptr(dg.col_indices), n, dg.num_edges,
+            rc = L.hc_solve(dg.row_offsets.data_ptr(), _lib.ptr(dg.col_indices), n, m,
                             _lib.MODE_CODES[args.mode], thr, solver.colors.data_ptr(),
                             solver.rec.data_ptr(), solver.max_rec, ctypes.byref(rounds),
                             solver.ws.data_ptr(), solver.ws.numel(), _lib.stream_handle(stream))
@@ -476,58 +505,74 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in zip(starts, stops)]
     total_ms = float(sum(step_ms))
-    ms_per_step = total_ms / args.steps
-    value = world * und * args.steps / (total_ms / 1e3)
-    clocks = clk.summary()
+    ms_per_step = total_ms / steps
+    value = und * steps / (total_ms / 1e3)
 
-    # hybrid vs the GPU's own pure data / topology modes (untimed for the headline)
+    # hybrid vs the GPU's own pure data / topology modes
     modes = {}
     if not args.skip_modes:
         for mode in ("hybrid", "data", "topo"):
             ts = []
-            for _ in range(3):
+            for _ in range(mode_reps):
                 flush.zero_()
                 ts.append(solver.run(mode, thr, fetch_records=False).seconds)
             modes[mode] = {"ms": min(ts) * 1e3, "und_edges_per_s": und / min(ts)}
+        # the paper's Plain data-driven baseline (IrGL worklist,
+        # atomic pushes, no ordering): hc_solve_plain, data mode
+        ts = []
+        for _ in range(mode_reps):
+            flush.zero_()
+            ts.append(solver.run("data", thr, fetch_records=False, plain=True).seconds)
+        modes["plain_data"] = {"ms": min(ts) * 1e3, "und_edges_per_s": und / min(ts),
+                               "what": "data-driven, warp-aggregated atomic pushes into unordered lists "
+                                       "(paper's IrGL Plain; bench-only)"}
         modes["hybrid_speedup_vs_data"] = modes["data"]["ms"] / modes["hybrid"]["ms"]
         modes["hybrid_speedup_vs_topo"] = modes["topo"]["ms"] / modes["hybrid"]["ms"]
+        modes["hybrid_speedup_vs_plain_data"] = modes["plain_data"]["ms"] / modes["hybrid"]["ms"]
+    del solver
 
     # e2e through the public API on pinned host buffers
     host = dg.to_host()
     pinned = hc.CsrGraph.pinned(host)
     e2e_ms = []
-    for i in range(args.warmup + args.steps):
+    for i in range(1 + e2e_steps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         colors, rep = hc.color_graph(pinned, hcfg)
         torch.cuda.synchronize()
-        if i >= args.warmup:
+        if i >= 1:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         assert rep.valid
+        del colors, rep
+    del pinned
     e2e_total = float(sum(e2e_ms))
-    e2e_value = world * und * args.steps / (e2e_total / 1e3)
 
     hbm, peak_kind = peaks()
-    achieved = b_alg / (ms_per_step / 1e3) / 1e9
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPU",
-        "config": {"workload": DESCRIPTIONS[args.config], "name": args.config, "mode": args.mode,
-                   "num_nodes": n, "num_undirected_edges": und, "rounds": R,
-                   "sum_wl_in": sum_visits, "l2": "flushed between timed steps (512 MiB write)",
-                   "parallelism": "single-gpu"},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": measured_traffic(args.config), "peak_kind": peak_kind,
-                     "kernel": "solve_kernel (+ bin preprocessing, whole hc_solve step)",
-                     "algorithmic_bytes_per_launch": b_alg},
-        "clocks": clocks,
-        "gpu_launches": launches_per_step * args.steps,
-        "modes": modes,
-        "e2e": {"value": e2e_value, "unit": UNIT,
-                "h2d_bytes_per_step": 8 * (n + 1) + 8 * dg.num_edges,
-                "d2h_bytes_per_step": 8 * n + 48 * R, "ms_per_step": e2e_total / args.steps},
+    achieved = b_survey / (ms_per_step / 1e3) / 1e9
+    own = b_own / (ms_per_step / 1e3) / 1e9
+    traffic = measured_traffic(name)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": traffic["bytes"] if traffic else None, "peak_kind": peak_kind,
+            "kernel": "solve_kernel (+ bin preprocessing, whole hc_solve step)",
+            "model": "SURVEY.md §8(d) per-round bytes (scan-based assign, 8 B packed (t,T))",
+            "algorithmic_bytes_per_launch": b_survey,
+            "own_model": {"bytes_per_launch": b_own, "achieved": own, "frac": own / hbm,
+                          "model": "bitmap assign + lower-neighbour resolve + per-solve winner pushes "
+                                   "(bench.py own_bytes)"}}
+    if traffic:
+        roof["dram"] = {"bytes_per_launch": traffic["bytes"], "ncu_ms": traffic["ns"] / 1e6,
+                        "achieved": traffic["bytes"] / (traffic["ns"] / 1e9) / 1e9 if traffic["ns"] else None,
+                        "frac": traffic["bytes"] / (traffic["ns"] / 1e9) / 1e9 / hbm if traffic["ns"] else None,
+                        "l2_hit_pct": traffic.get("l2_hit_pct"),
+                        "source": f"profiles/r02_{name}_traffic.csv (ncu, cold L2, serialised)"}
+    out = {
+        "workload": DESCRIPTIONS[name], "value": value, "unit": UNIT, "ms_per_step": ms_per_step,
+        "steps": steps, "warmup": warmup, "num_nodes": n, "num_undirected_edges": und, "rounds": R,
+        "sum_wl_in": int(recs[:, 2].sum()), "roofline": roof, "clocks": clk.summary(),
+        "gpu_launches": launches_per_step * steps, "modes": modes,
+        "e2e": {"value": und * e2e_steps / (e2e_total / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * (n + 1) + 8 * m, "d2h_bytes_per_step": 8 * n + 48 * R,
+                "ms_per_step": e2e_total / e2e_steps},
         "step_ms": step_ms,
     }
     if not args.skip_cpu:
@@ -535,9 +580,47 @@ def run_ours(args, cfg):
             ref = reference_module()
             warm_reference(ref)
             g = ref.CsrGraph(host.num_nodes, host.num_edges, host.row_offsets, host.col_indices)
-            line["cpu_baseline"] = cpu_sample(ref, g, args.cpu_budget, round_work(recs, st))
+            out["cpu_baseline"] = cpu_sample(ref, g, cpu_budget, round_work(recs, st))
+            del g
         except Exception as exc:  # reported, not fatal
-            line["cpu_baseline"] = {"value": None, "unavailable": repr(exc)}
+            out["cpu_baseline"] = {"value": None, "unavailable": repr(exc)}
+    del host, dg, flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(args, cfg):
+    import torch
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))  # N > 1: run_distributed
+    torch.cuda.set_device(local)
+    head = measure(args, args.config, args.steps, args.warmup, e2e_steps=args.steps, mode_reps=3,
+                   cpu_budget=args.cpu_budget)
+    line = {
+        "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (BASELINE generator spec, SURVEY.md Appendix C), built on the GPU",
+        "config": {"workload": head["workload"], "name": args.config, "mode": args.mode,
+                   "num_nodes": head["num_nodes"], "num_undirected_edges": head["num_undirected_edges"],
+                   "rounds": head["rounds"], "sum_wl_in": head["sum_wl_in"],
+                   "l2": "flushed between timed steps (512 MiB write)", "parallelism": "single-gpu"},
+        "roofline": head["roofline"], "clocks": head["clocks"], "gpu_launches": head["gpu_launches"],
+        "modes": head["modes"], "e2e": head["e2e"], "step_ms": head["step_ms"],
+    }
+    if "cpu_baseline" in head:
+        line["cpu_baseline"] = head["cpu_baseline"]
+    if args.all_configs:
+        # the other BASELINE configs (parity cases of the headline, reported
+        # like compare_backends.py:53-67: every mode, e2e, roofline, CPU solve)
+        line["configs"] = {}
+        for name in CONFIGS:
+            if name == args.config:
+                continue
+            line["configs"][name] = measure(args, name, min(args.steps, 5), 3, e2e_steps=2,
+                                            mode_reps=2 if name == "rmat26" else 3,
+                                            cpu_budget=args.cpu_budget_configs)
+            line["gpu_launches"] += line["configs"][name]["gpu_launches"]
     print(json.dumps(line), flush=True)
     return 0
 
@@ -552,7 +635,13 @@ def main():
     ap.add_argument("--mode", choices=("hybrid", "data", "topo"), default="hybrid")
     ap.add_argument("--skip-modes", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0,
+                    help="seconds of reference CPU solve for the headline config (grid: extrapolated)")
+    ap.add_argument("--cpu-budget-configs", type=float, default=60.0,
+                    help="the same for the other configs (full reference solves of C1/C3/C4 fit)")
+    ap.add_argument("--all-configs", dest="all_configs", action="store_true", default=True,
+                    help="also measure the other BASELINE configs under the line's 'configs' key (default)")
+    ap.add_argument("--headline-only", dest="all_configs", action="store_false")
     ap.add_argument("--share-gpu", action="store_true",
                     help="N>1 test knob: all ranks on cuda:0 over gloo (correctness only, not a bench)")
     args = ap.parse_args()

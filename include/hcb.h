@@ -150,6 +150,15 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
                    hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, int64_t *d_stats,
                    void *d_ws, size_t ws_bytes, void *stream);
 
+/* Bench-only "Plain" data-driven baseline (the paper's IrGL Plain,
+ * PAPER.md:268-283, 301-332): the same solve, but losers are pushed with
+ * warp-aggregated atomics into one dense, unordered list per degree bin
+ * (_kernels.pyx:114-118 without the sort of worklist.py:84), so data-driven
+ * rounds walk a fragmented list.  Same arguments and results as hc_solve. */
+int hc_solve_plain(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                   int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec,
+                   int64_t max_rec, int64_t *h_rounds, void *d_ws, size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------------ */
 /* Device-resident multi-GPU solve over NVLink peer memory (SURVEY.md   */
 /* §8(e); replaces driver.py:122-176 on a 1D vertex partition).  One    */
@@ -167,6 +176,13 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
 /*   h_bounds[world+1]: the partition (rank r owns [h_bounds[r],        */
 /*     h_bounds[r+1]); every rank passes the same array).  A boundary   */
 /*     word goes only to the ranks holding a neighbour of it.           */
+/*   The CSR is the rank's SHARD ("each GPU holds its  */
+/*     CSR rows"): d_row_offsets int64[hi-lo+1] (row r = node lo+r,     */
+/*     offsets into d_col_indices), d_col_indices int32[num_edges]      */
+/*     (global ids; num_edges = the shard's half-edges), rows as        */
+/*     build_csr makes them (hc_build_csr_rows).  num_nodes is global;  */
+/*     global_max_degree (the all-reduced max over ranks) fixes the     */
+/*     state-word width and kernel family, which every rank must share. */
 /*   hc_mg_solve: preprocessing (synchronous) + launch (asynchronous);  */
 /*     d_colors int64[hi-lo] receives the owned colors; every rank's    */
 /*     d_rec gets the same global records; ctas = 0: all resident CTAs; */
@@ -179,7 +195,7 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
 /* ------------------------------------------------------------------ */
 #define HC_IPC_HANDLE_BYTES 64
 size_t hc_mg_shared_bytes(int64_t num_nodes);
-size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t num_edges, int64_t lo, int64_t hi);
+size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t shard_edges, int64_t lo, int64_t hi);
 /* The one allocation the library makes: a shared region in its own
  * cudaMalloc allocation (zeroed), so it is IPC-exportable whatever the
  * caller's allocator does (e.g. virtual-memory segments).  Freed by
@@ -194,14 +210,16 @@ int hc_mg_ipc_close(void *d_ptr, int64_t offset);
 int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
                 int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                 int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
-                int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
+                int ctas, int64_t timeout_ms, int64_t global_max_degree, void *d_ws, size_t ws_bytes,
+                void *stream);
 /* hc_mg_solve == hc_mg_prepare + hc_mg_launch.  Ranks sharing one GPU
  * prepare all ranks first, then launch all (preprocessing kernels must not
  * queue behind another rank's persistent kernel). */
 int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
                   int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                   int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
-                  int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream);
+                  int ctas, int64_t timeout_ms, int64_t global_max_degree, void *d_ws, size_t ws_bytes,
+                  void *stream);
 int hc_mg_launch(void *d_ws, void *stream);
 int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream);
 /* How a rank's boundary words reach its peers (process-wide; tests /
@@ -255,6 +273,20 @@ int hc_build_csr(const int64_t *d_edges, int64_t num_pairs, int64_t num_nodes,
                  int64_t *d_row_offsets, int32_t *d_col_indices, int64_t *h_num_edges,
                  void *d_ws, size_t ws_bytes, void *stream);
 
+/* Rows [lo, hi) of build_csr (a multi-GPU shard): d_row_offsets
+ * int64[hi-lo+1] (row r = node lo+r), d_col_indices int32[dir_capacity] with
+ * global ids; dir_capacity >= the rows' directed entries before dedupe (their
+ * hc_edge_degrees sum), else HC_ERR_WORKSPACE.  Rows equal the same rows of
+ * hc_build_csr (graph.py:184-201).  hc_build_csr == rows [0, n). */
+size_t hc_build_csr_rows_workspace_bytes(int64_t num_nodes, int64_t lo, int64_t hi, int64_t dir_capacity);
+int hc_build_csr_rows(const int64_t *d_edges, int64_t num_pairs, int64_t num_nodes, int64_t lo, int64_t hi,
+                      int64_t dir_capacity, int64_t *d_row_offsets, int32_t *d_col_indices,
+                      int64_t *h_num_edges, void *d_ws, size_t ws_bytes, void *stream);
+/* d_deg int64[n]: per node the half-edges of the pair list with loops
+ * dropped and duplicates kept (graph.py:191-192 before np.unique) -- the
+ * prefix the multi-GPU partition is cut on before any shard exists. */
+int hc_edge_degrees(const int64_t *d_edges, int64_t num_pairs, int64_t num_nodes, int64_t *d_deg, void *stream);
+
 /* Synthetic edge streams (bit-identical to
  * oracle/ipgc_oracle.c orc_gen_*).  d_edges int64[2*m]. */
 int hc_gen_grid(int64_t rows, int64_t cols, int64_t *d_edges, void *stream);
@@ -266,6 +298,11 @@ int hc_gen_rmat(int scale, int64_t num_pairs, uint64_t seed, int64_t *d_edges, v
  * HC_ERR_UNCOLORED if any entry < 1. */
 int hc_verify(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
               const int64_t *d_colors, int64_t *d_acc, int64_t *h_bad, void *stream);
+/* verify_coloring over a shard's rows [lo, hi) (row offsets as in
+ * hc_build_csr_rows; d_colors indexed by global id) -- the multi-GPU
+ * RunReport sums it over ranks. */
+int hc_verify_rows(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t lo, int64_t hi,
+                   const int64_t *d_colors, int64_t *d_acc, int64_t *h_bad, void *stream);
 /* d_acc: int64[2] device scratch */
 int hc_colors_used(const int64_t *d_colors, int64_t num_nodes, int64_t *d_acc, int64_t *h_used,
                    void *stream);

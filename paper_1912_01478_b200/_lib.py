@@ -76,6 +76,7 @@ _SIGS = {
     "hc_solve_set_formats": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "hc_solve_set_small": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
+    "hc_solve_plain": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_stats": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, _p, ctypes.c_size_t, _p]),
     "hc_mg_shared_bytes": (ctypes.c_size_t, [_i64]),
     "hc_mg_workspace_bytes": (ctypes.c_size_t, [_i64, _i64, _i64, _i64]),
@@ -85,11 +86,11 @@ _SIGS = {
     "hc_mg_ipc_import": (ctypes.c_int, [_p, _i64, _p]),
     "hc_mg_ipc_close": (ctypes.c_int, [_p, _i64]),
     "hc_mg_solve": (ctypes.c_int, [_p, _p, _i64, _i64, _p, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
-                                   _i64, _p, _p, _i64, ctypes.c_int, _i64, _p, ctypes.c_size_t, _p]),
+                                   _i64, _p, _p, _i64, ctypes.c_int, _i64, _i64, _p, ctypes.c_size_t, _p]),
     "hc_mg_wait": (ctypes.c_int, [_p, _p, _p]),
     "hc_mg_set_exchange": (ctypes.c_int, [ctypes.c_int]),
     "hc_mg_prepare": (ctypes.c_int, [_p, _p, _i64, _i64, _p, ctypes.c_int, ctypes.c_int, _p, ctypes.c_int,
-                                     _i64, _p, _p, _i64, ctypes.c_int, _i64, _p, ctypes.c_size_t, _p]),
+                                     _i64, _p, _p, _i64, ctypes.c_int, _i64, _i64, _p, ctypes.c_size_t, _p]),
     "hc_mg_launch": (ctypes.c_int, [_p, _p]),
     "hc_dist_boundary": (ctypes.c_int, [_p, _p, _i64, _i64, _p, _p]),
     "hc_dist_assign": (ctypes.c_int, [_p, _p, _p, _p, _i64, _i64, _p, _p, _p, _p, _p]),
@@ -100,6 +101,10 @@ _SIGS = {
     "hc_push_bench": (ctypes.c_int, [_i64, _i64, ctypes.c_int, _p, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_build_csr_workspace_bytes": (ctypes.c_size_t, [_i64, _i64]),
     "hc_build_csr": (ctypes.c_int, [_p, _i64, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "hc_build_csr_rows_workspace_bytes": (ctypes.c_size_t, [_i64, _i64, _i64, _i64]),
+    "hc_build_csr_rows": (ctypes.c_int, [_p, _i64, _i64, _i64, _i64, _i64, _p, _p, _p, _p, ctypes.c_size_t, _p]),
+    "hc_edge_degrees": (ctypes.c_int, [_p, _i64, _i64, _p, _p]),
+    "hc_verify_rows": (ctypes.c_int, [_p, _p, _i64, _i64, _p, _p, _p, _p]),
     "hc_gen_grid": (ctypes.c_int, [_i64, _i64, _p, _p]),
     "hc_gen_er": (ctypes.c_int, [_i64, _i64, ctypes.c_uint64, _p, _p]),
     "hc_gen_rmat": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_uint64, _p, _p]),

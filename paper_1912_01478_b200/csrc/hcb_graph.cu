@@ -172,8 +172,10 @@ static int exclusive_scan(const unsigned *in, long long count, unsigned long lon
 }
 
 // ------------------------------------------------------------- csr build
-__global__ void degree_kernel(const longlong2 *edges, long long m, long long n, unsigned *deg,
-                              unsigned *status) {
+// Rows [lo, hi) of the CSR (the whole graph: lo = 0, hi = n; a multi-GPU
+// shard: the rank's owned range, with global column ids).  Row r = node lo+r.
+__global__ void degree_kernel(const longlong2 *edges, long long m, long long n, long long lo, long long hi,
+                              unsigned *deg, unsigned *status) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (long long)gridDim.x * blockDim.x) {
         const longlong2 e = edges[k];
@@ -182,20 +184,52 @@ __global__ void degree_kernel(const longlong2 *edges, long long m, long long n, 
             continue;
         }
         if (e.x == e.y) continue;  // graph.py:192
-        atomicAdd(&deg[e.x], 1u);
-        atomicAdd(&deg[e.y], 1u);
+        if (e.x >= lo && e.x < hi) atomicAdd(&deg[e.x - lo], 1u);
+        if (e.y >= lo && e.y < hi) atomicAdd(&deg[e.y - lo], 1u);
     }
 }
 
-__global__ void scatter_kernel(const longlong2 *edges, long long m, long long n,
+__global__ void scatter_kernel(const longlong2 *edges, long long m, long long n, long long lo, long long hi,
                                unsigned long long *cur, int *tmp) {
     for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
          k += (long long)gridDim.x * blockDim.x) {
         const longlong2 e = edges[k];
         if (e.x < 0 || e.x >= n || e.y < 0 || e.y >= n || e.x == e.y) continue;
-        tmp[atomicAdd(&cur[e.x], 1ull)] = (int)e.y;  // graph.py:191 both directions
-        tmp[atomicAdd(&cur[e.y], 1ull)] = (int)e.x;
+        // graph.py:191 both directions
+        if (e.x >= lo && e.x < hi) tmp[atomicAdd(&cur[e.x - lo], 1ull)] = (int)e.y;
+        if (e.y >= lo && e.y < hi) tmp[atomicAdd(&cur[e.y - lo], 1ull)] = (int)e.x;
     }
+}
+
+// raw half-edge count per node (loops dropped, duplicates counted): the
+// multi-GPU partition is cut on its prefix before any rank builds its shard
+__global__ void raw_degree_kernel(const longlong2 *edges, long long m, long long n,
+                                  unsigned long long *deg) {
+    for (long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x; k < m;
+         k += (long long)gridDim.x * blockDim.x) {
+        const longlong2 e = edges[k];
+        if (e.x < 0 || e.x >= n || e.y < 0 || e.y >= n || e.x == e.y) continue;
+        atomicAdd(&deg[e.x], 1ull);
+        atomicAdd(&deg[e.y], 1ull);
+    }
+}
+
+// multi-GPU verify of a shard: edges u<v of the owned rows with equal colors
+// or an uncolored u, colors indexed by global id (driver.py:188-204)
+__global__ void verify_rows_kernel(const long long *ro, const int *ci, long long lo, long long nrows,
+                                   const long long *colors, unsigned long long *acc) {
+    const unsigned lane = lane_id();
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    unsigned long long bad = 0;
+    for (long long r = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < nrows; r += nwarps) {
+        const long long u = lo + r, cu = colors[u];
+        for (long long k = ro[r] + lane; k < ro[r + 1]; k += 32) {
+            const long long v = ci[k];
+            if (u < v && (cu == colors[v] || cu == 0)) ++bad;
+        }
+    }
+    bad = warp_sum(bad);
+    if (lane == 0 && bad) atomicAdd(acc, bad);
 }
 
 constexpr int SMALL_ROW = 64;
@@ -478,21 +512,23 @@ struct CsrLayout {
     int big_ctas;
 };
 
-static CsrLayout csr_layout(long long n, long long m) {
+// n = the graph's node count (bitmap width), rows = rows built, dir = the
+// directed (pre-dedupe) entries of those rows (2m for the whole graph)
+static CsrLayout csr_layout(long long n, long long rows, long long dir) {
     CsrLayout L;
     size_t o = 0;
     L.big_ctas = num_sms() > 0 ? num_sms() : 148;
-    L.deg = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
-    L.off = o; o = align_up(o + 8 * (size_t)(n + 1), 256);
-    L.cur = o; o = align_up(o + 8 * (size_t)(n + 1), 256);
-    L.tmp = o; o = align_up(o + 4 * (size_t)(2 * m + 1), 256);
-    L.uniq = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
-    L.ro_u = o; o = align_up(o + 8 * (size_t)(n + 1), 256);
-    L.rows = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
+    L.deg = o; o = align_up(o + 4 * (size_t)(rows + 1), 256);
+    L.off = o; o = align_up(o + 8 * (size_t)(rows + 1), 256);
+    L.cur = o; o = align_up(o + 8 * (size_t)(rows + 1), 256);
+    L.tmp = o; o = align_up(o + 4 * (size_t)(dir + 1), 256);
+    L.uniq = o; o = align_up(o + 4 * (size_t)(rows + 1), 256);
+    L.ro_u = o; o = align_up(o + 8 * (size_t)(rows + 1), 256);
+    L.rows = o; o = align_up(o + 4 * (size_t)(rows + 1), 256);
     L.status = o; o = align_up(o + 256, 256);
     L.bitmaps = o; o = align_up(o + 4 * (size_t)((n + 31) / 32) * (size_t)L.big_ctas, 256);
-    L.scan = o; o = align_up(o + scan_scratch_bytes(n + 1), 256);
-    L.part = o; o = align_up(o + part_scratch_bytes(2, n), 256);
+    L.scan = o; o = align_up(o + scan_scratch_bytes(rows + 1), 256);
+    L.part = o; o = align_up(o + part_scratch_bytes(2, rows), 256);
     L.total = o;
     return L;
 }
@@ -537,22 +573,29 @@ int hc_gen_rmat(int scale, int64_t m, uint64_t seed, int64_t *d_edges, void *str
 size_t hc_build_csr_workspace_bytes(int64_t n, int64_t m) {
     if (n < 0) n = 0;
     if (m < 0) m = 0;
-    return csr_layout(n, m).total;
+    return csr_layout(n, n, 2 * m).total;
 }
 
-int hc_build_csr(const int64_t *d_edges, int64_t m, int64_t n, int64_t *d_row_offsets,
-                 int32_t *d_col_indices, int64_t *h_num_edges, void *d_ws, size_t ws_bytes,
-                 void *stream) {
-    HC_REQUIRE(n >= 0 && n < 0x7fffffffLL && m >= 0 && h_num_edges && d_row_offsets, HC_ERR_INVALID,
-               "build_csr: bad arguments");
+size_t hc_build_csr_rows_workspace_bytes(int64_t n, int64_t lo, int64_t hi, int64_t dir_capacity) {
+    if (n < 0) n = 0;
+    const long long rows = hi > lo ? hi - lo : 0;
+    return csr_layout(n, rows, dir_capacity < 0 ? 0 : dir_capacity).total;
+}
+
+int hc_build_csr_rows(const int64_t *d_edges, int64_t m, int64_t n, int64_t lo, int64_t hi,
+                      int64_t dir_capacity, int64_t *d_row_offsets, int32_t *d_col_indices,
+                      int64_t *h_num_edges, void *d_ws, size_t ws_bytes, void *stream) {
+    HC_REQUIRE(n >= 0 && n < 0x7fffffffLL && m >= 0 && h_num_edges && d_row_offsets && lo >= 0 && lo <= hi &&
+                   hi <= n && dir_capacity >= 0, HC_ERR_INVALID, "build_csr: bad arguments");
     cudaStream_t st = as_stream(stream);
+    const long long rows = hi - lo;
     *h_num_edges = 0;
-    if (n == 0 || m == 0) {  // graph.py:188-189
-        HC_CUDA_TRY(cudaMemsetAsync(d_row_offsets, 0, 8 * (size_t)(n + 1), st));
+    if (rows == 0 || m == 0) {  // graph.py:188-189
+        HC_CUDA_TRY(cudaMemsetAsync(d_row_offsets, 0, 8 * (size_t)(rows + 1), st));
         HC_CUDA_TRY(cudaStreamSynchronize(st));
         return HC_OK;
     }
-    const CsrLayout L = csr_layout(n, m);
+    const CsrLayout L = csr_layout(n, rows, dir_capacity);
     HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
                "build_csr: workspace %zu < required %zu", ws_bytes, L.total);
     char *ws = reinterpret_cast<char *>(d_ws);
@@ -562,51 +605,92 @@ int hc_build_csr(const int64_t *d_edges, int64_t m, int64_t n, int64_t *d_row_of
     int *tmp = reinterpret_cast<int *>(ws + L.tmp);
     unsigned *uniq = reinterpret_cast<unsigned *>(ws + L.uniq);
     unsigned long long *ro = reinterpret_cast<unsigned long long *>(d_row_offsets);
-    int *rows = reinterpret_cast<int *>(ws + L.rows);
+    int *rowlist = reinterpret_cast<int *>(ws + L.rows);
     unsigned *status = reinterpret_cast<unsigned *>(ws + L.status);
     unsigned *bitmaps = reinterpret_cast<unsigned *>(ws + L.bitmaps);
     const longlong2 *edges = reinterpret_cast<const longlong2 *>(d_edges);
 
-    HC_CUDA_TRY(cudaMemsetAsync(deg, 0, 4 * (size_t)(n + 1), st));
+    HC_CUDA_TRY(cudaMemsetAsync(deg, 0, 4 * (size_t)(rows + 1), st));
     HC_CUDA_TRY(cudaMemsetAsync(status, 0, 256, st));
     HC_CUDA_TRY(cudaMemsetAsync(bitmaps, 0, 4 * (size_t)((n + 31) / 32) * (size_t)L.big_ctas, st));
-    degree_kernel<<<grid_cap(m, BLOCK), BLOCK, 0, st>>>(edges, m, n, deg, status);
+    degree_kernel<<<grid_cap(m, BLOCK), BLOCK, 0, st>>>(edges, m, n, lo, hi, deg, status);
     HC_CHECK_LAUNCH();
-    int rc = exclusive_scan(deg, n, off, ws + L.scan, st);
+    int rc = exclusive_scan(deg, rows, off, ws + L.scan, st);
     if (rc) return rc;
-    HC_CUDA_TRY(cudaMemcpyAsync(cur, off, 8 * (size_t)n, cudaMemcpyDeviceToDevice, st));
-    scatter_kernel<<<grid_cap(m, BLOCK), BLOCK, 0, st>>>(edges, m, n, cur, tmp);
+    unsigned long long dir = 0;
+    unsigned h_status = 0;
+    HC_CUDA_TRY(cudaMemcpyAsync(&dir, off + rows, sizeof dir, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaMemcpyAsync(&h_status, status, sizeof h_status, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
+    HC_REQUIRE(!h_status, HC_ERR_INVALID, "edge endpoint outside declared node range");  // graph.py:39-42
+    HC_REQUIRE((long long)dir <= dir_capacity, HC_ERR_WORKSPACE,
+               "build_csr: rows [%lld, %lld) hold %llu directed entries > capacity %lld", (long long)lo,
+               (long long)hi, dir, (long long)dir_capacity);
+    HC_CUDA_TRY(cudaMemcpyAsync(cur, off, 8 * (size_t)rows, cudaMemcpyDeviceToDevice, st));
+    scatter_kernel<<<grid_cap(m, BLOCK), BLOCK, 0, st>>>(edges, m, n, lo, hi, cur, tmp);
     HC_CHECK_LAUNCH();
-    sort_small_rows_kernel<<<grid_cap(n, BLOCK / 32), BLOCK, 0, st>>>(off, n, tmp, uniq);
+    sort_small_rows_kernel<<<grid_cap(rows, BLOCK / 32), BLOCK, 0, st>>>(off, rows, tmp, uniq);
     HC_CHECK_LAUNCH();
     unsigned long long *totals = nullptr;
-    rc = ordered_partition<2>(n, RowBin{off}, EmitRow{}, rows, ws + L.part, &totals, st);
+    rc = ordered_partition<2>(rows, RowBin{off}, EmitRow{}, rowlist, ws + L.part, &totals, st);
     if (rc) return rc;
     unsigned long long h_tot[2];
     HC_CUDA_TRY(cudaMemcpyAsync(h_tot, totals, sizeof h_tot, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
     if (h_tot[0]) {
         sort_mid_rows_kernel<<<grid_cap((long long)h_tot[0], 1), MID_THREADS, 0, st>>>(
-            off, rows, (long long)h_tot[0], tmp, uniq);
+            off, rowlist, (long long)h_tot[0], tmp, uniq);
         HC_CHECK_LAUNCH();
     }
     if (h_tot[1]) {
         const int ctas = (int)std::min<long long>((long long)h_tot[1], L.big_ctas);
-        sort_big_rows_kernel<<<ctas, BLOCK, 0, st>>>(off, rows + h_tot[0], (long long)h_tot[1], n, tmp,
+        sort_big_rows_kernel<<<ctas, BLOCK, 0, st>>>(off, rowlist + h_tot[0], (long long)h_tot[1], n, tmp,
                                                      uniq, bitmaps);
         HC_CHECK_LAUNCH();
     }
-    rc = exclusive_scan(uniq, n, ro, ws + L.scan, st);
+    rc = exclusive_scan(uniq, rows, ro, ws + L.scan, st);
     if (rc) return rc;
-    compact_kernel<<<grid_cap(n, BLOCK / 32), BLOCK, 0, st>>>(off, ro, tmp, n, d_col_indices);
+    compact_kernel<<<grid_cap(rows, BLOCK / 32), BLOCK, 0, st>>>(off, ro, tmp, rows, d_col_indices);
     HC_CHECK_LAUNCH();
-    unsigned h_status = 0;
     long long total = 0;
-    HC_CUDA_TRY(cudaMemcpyAsync(&h_status, status, sizeof h_status, cudaMemcpyDeviceToHost, st));
-    HC_CUDA_TRY(cudaMemcpyAsync(&total, ro + n, sizeof total, cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaMemcpyAsync(&total, ro + rows, sizeof total, cudaMemcpyDeviceToHost, st));
     HC_CUDA_TRY(cudaStreamSynchronize(st));
-    HC_REQUIRE(!h_status, HC_ERR_INVALID, "edge endpoint outside declared node range");  // graph.py:39-42
     *h_num_edges = total;
+    return HC_OK;
+}
+
+int hc_build_csr(const int64_t *d_edges, int64_t m, int64_t n, int64_t *d_row_offsets,
+                 int32_t *d_col_indices, int64_t *h_num_edges, void *d_ws, size_t ws_bytes,
+                 void *stream) {
+    HC_REQUIRE(n >= 0 && n < 0x7fffffffLL && m >= 0, HC_ERR_INVALID, "build_csr: bad arguments");
+    return hc_build_csr_rows(d_edges, m, n, 0, n, 2 * m, d_row_offsets, d_col_indices, h_num_edges, d_ws,
+                             ws_bytes, stream);
+}
+
+int hc_edge_degrees(const int64_t *d_edges, int64_t m, int64_t n, int64_t *d_deg, void *stream) {
+    HC_REQUIRE(n >= 0 && m >= 0 && d_deg, HC_ERR_INVALID, "edge_degrees: bad arguments");
+    cudaStream_t st = as_stream(stream);
+    HC_CUDA_TRY(cudaMemsetAsync(d_deg, 0, 8 * (size_t)std::max<int64_t>(n, 1), st));
+    if (m > 0 && n > 0) {
+        raw_degree_kernel<<<grid_cap(m, BLOCK), BLOCK, 0, st>>>((const longlong2 *)d_edges, m, n,
+                                                                (unsigned long long *)d_deg);
+        HC_CHECK_LAUNCH();
+    }
+    return HC_OK;
+}
+
+int hc_verify_rows(const int64_t *d_ro, const int32_t *d_ci, int64_t lo, int64_t hi, const int64_t *d_colors,
+                   int64_t *d_acc, int64_t *h_bad, void *stream) {
+    HC_REQUIRE(lo >= 0 && hi >= lo && d_acc && h_bad, HC_ERR_INVALID, "verify_rows: bad arguments");
+    cudaStream_t st = as_stream(stream);
+    HC_CUDA_TRY(cudaMemsetAsync(d_acc, 0, sizeof(int64_t), st));
+    if (hi > lo) {
+        verify_rows_kernel<<<grid_cap(hi - lo, BLOCK / 32), BLOCK, 0, st>>>(
+            (const long long *)d_ro, d_ci, lo, hi - lo, (const long long *)d_colors, (unsigned long long *)d_acc);
+        HC_CHECK_LAUNCH();
+    }
+    HC_CUDA_TRY(cudaMemcpyAsync(h_bad, d_acc, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    HC_CUDA_TRY(cudaStreamSynchronize(st));
     return HC_OK;
 }
 

@@ -134,6 +134,7 @@ struct Ctrl {
     unsigned long long g_wl, g_conf;
     unsigned abort;
     unsigned pad2;
+    unsigned long long plain_cnt[2][NSEG_BINS];  // Plain variant: dense list sizes per parity and bin
     unsigned segcnt[2][NSEG_BINS][MAXSEG];       // [parity][bin][segment] loser counts
 };
 
@@ -190,6 +191,13 @@ struct Params {
     long long *stats;          // optional int64[max_rec][2]: (assign edges, resolve lower edges)
     HubAcc *hub_acc;           // MAX_SPLIT_SLOTS merge slots (zeroed; reset by their last slice)
     unsigned *fmt_overflow;    // set when a tentative color does not fit the state word
+    // forbidden-color bitmaps (single GPU): fb0[u] bit c-1 = a committed
+    // neighbour of u has color c (c <= 32); colors 33..deg(u)+1 in
+    // fbx[(ro[u] >> 5) + (c - 33) / 32].  Winners set the bits of their color
+    // in every neighbour once, when they commit; assign is then the mex of the
+    // node's own bitmap instead of a scan of its adjacency.
+    unsigned *fb0;
+    unsigned *fbx;
     long long lo, nown;        // owned node range [lo, lo + nown) (single GPU: 0, n)
     // multi-GPU (Fmt::mg) only
     const unsigned char *bnd;  // per owned node: bit q = rank q reads this word (global id index)
@@ -319,6 +327,25 @@ __device__ __forceinline__ void seg_put(const Params &P, int np, int bin, unsign
     if constexpr (MG) s_wl_acc += cnt;
 }
 
+// Plain variant: push of a loser with cooperative conversion (one atomic per
+// warp, IrGL's warp-aggregated push) into the bin's dense next list, in
+// whatever order the warps arrive.  Called by the whole warp.
+template <class F>
+__device__ __forceinline__ void plain_push(const Params &P, int np, int bin, bool take, int u,
+                                           unsigned long long od) {
+    const unsigned m = __ballot_sync(FULL, take);
+    if (!m) return;
+    const int leader = __ffs(m) - 1;
+    unsigned long long base = 0;
+    if (lane_id() == (unsigned)leader) base = atomicAdd(&P.ctrl->plain_cnt[np][bin], (unsigned long long)__popc(m));
+    base = __shfl_sync(FULL, base, leader);
+    if (take) {
+        const unsigned long long pos = base + __popc(m & lanemask_lt());
+        dyn_list(P, np, bin)[pos] = u;
+        if constexpr (!F::small) dyn_od(P, np, bin)[pos] = od;
+    }
+}
+
 // set by any thread of the CTA that issued NVLink stores in the current
 // phase: only such CTAs need the system-scope fence before the next barrier
 __shared__ unsigned s_mirrored;
@@ -421,12 +448,17 @@ __device__ bool mg_sync(const Params &P, SMT &sm, unsigned long long epoch, int 
 //   MG          multi-GPU (hc_mg_solve): this rank owns [lo, lo+nown); writes
 //               of owned boundary words are mirrored into every peer's replica
 //   SMALL       only bin-0 nodes (see SmemT)
-template <typename XT, typename CT, bool MG = false, bool SMALL = false>
+//   PLAIN       bench-only "Plain" data-driven baseline (the paper's IrGL Plain,
+//               PAPER.md:268-283): losers are pushed with warp-aggregated
+//               atomics into one dense, unordered list per bin instead of the
+//               order-preserving segmented compaction (_kernels.pyx:114-118)
+template <typename XT, typename CT, bool MG = false, bool SMALL = false, bool PLAIN = false>
 struct Fmt {
     using xt = XT;
     using ct = CT;
     static constexpr bool mg = MG;
     static constexpr bool small = SMALL;
+    static constexpr bool plain = PLAIN;
 };
 using F32 = Fmt<unsigned, int>;
 using F16 = Fmt<unsigned short, int>;
@@ -444,6 +476,14 @@ using SMF32 = Fmt<unsigned, int, true, true>;
 using SMF16 = Fmt<unsigned short, int, true, true>;
 using SMF16D = Fmt<unsigned short, short, true, true>;
 using SMF32D = Fmt<unsigned, short, true, true>;
+using PF32 = Fmt<unsigned, int, false, false, true>;
+using PF16 = Fmt<unsigned short, int, false, false, true>;
+using PF16D = Fmt<unsigned short, short, false, false, true>;
+using PF32D = Fmt<unsigned, short, false, false, true>;
+using PSF32 = Fmt<unsigned, int, false, true, true>;
+using PSF16 = Fmt<unsigned short, int, false, true, true>;
+using PSF16D = Fmt<unsigned short, short, false, true, true>;
+using PSF32D = Fmt<unsigned, short, false, true, true>;
 
 // committed flag / color mask of the format's state word; words are kept
 // zero-extended in registers, so no conversion on load or store
@@ -543,6 +583,67 @@ __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
     if ((x & FB<F>) && c <= 64u) mask |= 1ull << (c - 1u);
 }
 
+// ---------------------------------------------------- forbidden-color bitmaps
+// A node's bitmap covers colors 1..deg+1 (its mex is <= deg+1,
+// _kernels.pyx:49-56): word fb0[u] for colors 1..32, then floor(deg/32) words
+// fbx[(ro[u] >> 5) ...] for colors 33.. -- disjoint per node because
+// (ro[u+1] >> 5) - (ro[u] >> 5) >= floor(deg(u) / 32), so no per-node offset
+// array is needed.  Bits are only ever set (by winners, in resolve), and assign
+// of round t reads them after the grid barrier that ends round t-1: the bitmap
+// then holds exactly the colors committed before round t, i.e. the
+// reference's colors_read snapshot restricted to u's neighbours.
+template <class F>
+constexpr bool FBM = !F::mg;  // the multi-GPU solve keeps the adjacency-scan assign
+
+// winner's color c into neighbour v's bitmap (fire-and-forget RED)
+template <typename OffT>
+__device__ __forceinline__ void fb_push(const Params &P, const OffT *ro, int v, unsigned c) {
+    if (c <= 32u) {
+        atomicOr(P.fb0 + v, 1u << (c - 1u));
+        return;
+    }
+    const long long b = (long long)ro[v], e = (long long)ro[v + 1];
+    if ((long long)c > e - b + 1) return;  // c > deg(v)+1 is never v's mex
+    atomicOr(P.fbx + (b >> 5) + ((c - 33u) >> 5), 1u << ((c - 33u) & 31u));
+}
+
+// mex of node u's bitmap, one thread (w0 = fb0[u] already loaded)
+template <typename OffT>
+__device__ __forceinline__ unsigned fb_mex_thread(const Params &P, const OffT *ro, int u, unsigned w0) {
+    if (w0 != FULL) return (unsigned)__ffs(~w0);
+    const unsigned *x = P.fbx + ((long long)ro[u] >> 5);
+    for (unsigned j = 0;; ++j) {  // a zero bit exists among colors 1..deg+1
+        const unsigned w = x[j];
+        if (w != FULL) return 32u * j + 32u + (unsigned)__ffs(~w);
+    }
+}
+
+// mex of a hub / CTA-granularity node's bitmap, whole CTA
+template <typename OffT, class SMT>
+__device__ unsigned fb_mex_cta(const Params &P, const OffT *ro, int u, SMT &sm) {
+    const unsigned w0 = P.fb0[u];
+    if (w0 != FULL) return (unsigned)__ffs(~w0);
+    const unsigned *x = P.fbx + ((long long)ro[u] >> 5);
+    const long long nw = ((long long)ro[u + 1] >> 5) - ((long long)ro[u] >> 5);
+    for (long long j0 = 0;; j0 += BLOCK) {
+        if (threadIdx.x == 0) sm.hub_first = 0x7fffffff;
+        __syncthreads();
+        const long long j = j0 + threadIdx.x;
+        if (j < nw && x[j] != FULL) atomicMin(&sm.hub_first, (int)(j - j0));
+        __syncthreads();
+        const int f = sm.hub_first;
+        __syncthreads();
+        if (f != 0x7fffffff) return 32u * (unsigned)(j0 + f) + 32u + (unsigned)__ffs(~x[j0 + f]);
+    }
+}
+
+// a winner of the CTA-granularity paths pushes its color into every neighbour
+template <typename OffT, class F>
+__device__ __forceinline__ void fb_push_row_cta(const Params &P, const OffT *ro, int u, unsigned c) {
+    const long long b = ro[u], e = ro[u + 1];
+    for (long long k = b + threadIdx.x; k < e; k += BLOCK) fb_push(P, ro, colget<F, true>(P, k, u), c);
+}
+
 // ------------------------------------------------------------------ groups
 // Warp-level mex over window(s) above color 64, for a node whose colors
 // 1..64 are all taken (rare): whole warp, one node.
@@ -578,7 +679,8 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
                                            unsigned long long hi, bool topo, int *out,
                                            unsigned long long *out_od, unsigned *out_cnt, unsigned *bm,
                                            unsigned &seg_hint,
-                                           unsigned long long &my_conf, unsigned long long *my_edges) {
+                                           unsigned long long &my_conf, unsigned long long *my_edges,
+                                           int np_plain = 0, int bin_plain = 0) {
     const unsigned lane = lane_id();
     const unsigned sub = lane % G, gi = lane / G;
     const unsigned long long v = v0 + gi;
@@ -597,6 +699,31 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     }
     const long long b = u >= 0 ? (long long)(od >> 16) : 0;
     const long long e = u >= 0 ? b + (long long)(od & 0xffffull) : 0;
+    if constexpr (PHASE == 0 && FBM<F>) {
+        // mex of the node's forbidden-color bitmap: word fb0[u] (one
+        // transaction per group), the extension words only if colors 1..32
+        // are all taken -- G words per step, first non-full word of the group
+        const unsigned w0 = u >= 0 ? P.fb0[u] : 0u;
+        bool need = u >= 0 && w0 == FULL;
+        unsigned T = (u >= 0 && !need) ? (unsigned)__ffs(~w0) : 0u;
+        const unsigned *fx = P.fbx + (b >> 5);
+        for (unsigned j0 = 0; __any_sync(FULL, need); j0 += G) {
+            const unsigned w = need ? fx[j0 + sub] : FULL;
+            const unsigned bal = __ballot_sync(FULL, need && w != FULL);
+            const unsigned gb = G == 32 ? bal : (bal >> (gi * G)) & ((1u << (G & 31)) - 1u);
+            const int f = gb ? __ffs(gb) - 1 : 0;
+            const unsigned wf = __shfl_sync(FULL, w, (G == 32 ? 0 : (int)(gi * G)) + f);
+            if (need && gb) {
+                T = 32u * (j0 + (unsigned)f) + 32u + (unsigned)__ffs(~wf);
+                need = false;
+            }
+        }
+        if (sub == 0 && u >= 0) {
+            xput<F>(P, u, T);
+            if (STATS) my_edges[0] += e - b;
+        }
+        return;
+    }
     unsigned iters = (unsigned)((e - b + 4 * G - 1) / (4 * G));
     iters = __reduce_max_sync(FULL, iters);
     unsigned long long mask = 0, mask2 = 0;  // colors 1..64, 65..128 (mask2: G == 32 only)
@@ -704,11 +831,25 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             my_conf += cnt;
             if (STATS) my_edges[1] += low;
             if (cnt) {
-                const unsigned pos = atomicAdd(out_cnt, 1u);
-                out[pos] = u;
-                out_od[pos] = od;
+                if constexpr (!F::plain) {
+                    const unsigned pos = atomicAdd(out_cnt, 1u);
+                    out[pos] = u;
+                    out_od[pos] = od;
+                }
             } else {
                 xput<F>(P, u, xu | FB<F>);
+            }
+        }
+        if constexpr (F::plain) plain_push<F>(P, np_plain, bin_plain, sub == 0 && u >= 0 && cnt != 0, u, od);
+        if constexpr (FBM<F>) {
+            if (u >= 0 && cnt == 0) {  // group-uniform: the winner's color goes into every neighbour's bitmap
+                if constexpr (G < 32) {  // the first column batch is the whole adjacency
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (nb[q] != 0x7fffffff) fb_push(P, ro, nb[q], xu);
+                } else {
+                    for (long long k = b + sub; k < e; k += G) fb_push(P, ro, colget<F>(P, k, u), xu);
+                }
             }
         }
     }
@@ -847,15 +988,32 @@ struct TileA {
     int u[NP];
     OffT rb[NP], re[NP];
     unsigned xu[NP];
+    unsigned w0[NP];  // forbidden-color word of the node (bitmap assign)
 };
 
-template <typename OffT, class F, int NP, int PHASE>
+template <typename OffT, class F, int NP, int PHASE, bool STATS>
 __device__ __forceinline__ void tile_issue(const Params &P, const OffT *ro, const RoundCfg &rc,
                                            const unsigned *prefix, unsigned long long base,
                                            unsigned long long hi, TileA<OffT, NP> &a, unsigned &seg) {
     // seg: segment-walk hint carried across the tiles of a chunk (positions grow)
     const List &L = rc.L[0];
     const bool topo = rc.topo, ident = rc.ident;
+    if constexpr (PHASE == 0 && FBM<F> && !STATS) {
+        // bitmap assign: list entry, then the activity word (topology sweep)
+        // and the forbidden-color word together -- no row offsets, no columns
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            const unsigned long long v = base + (unsigned long long)j * BLOCK + threadIdx.x;
+            a.u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : ld_entry(L.base + list_index_walk(L, prefix, v, seg)))
+                            : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            a.xu[j] = (topo && a.u[j] >= 0) ? xget<F>(P, a.u[j]) : 0u;
+            a.w0[j] = a.u[j] >= 0 ? P.fb0[a.u[j]] : 0u;
+        }
+        return;
+    }
     // bin-0-only graphs (grids, meshes) read the row offsets: their lists are
     // nearly id-ordered, so the offsets are almost contiguous, and a 4-byte
     // list entry beats the 12-byte (id, od) pair (grid4096 data 843 vs 969 ms)
@@ -886,16 +1044,33 @@ __device__ __forceinline__ void tile_issue(const Params &P, const OffT *ro, cons
     }
 #pragma unroll
     for (int j = 0; j < NP; ++j) a.xu[j] = ((topo || PHASE == 1) && a.u[j] >= 0) ? xget<F>(P, a.u[j]) : 0u;
+    if constexpr (PHASE == 0 && FBM<F>) {  // STATS builds (row offsets loaded for the edge count)
+#pragma unroll
+        for (int j = 0; j < NP; ++j) a.w0[j] = a.u[j] >= 0 ? P.fb0[a.u[j]] : 0u;
+    }
 }
 
 template <typename OffT, class F, bool STATS, int PHASE, int NP>
-__device__ __forceinline__ void tile_finish(const Params &P, const RoundCfg &rc, TileA<OffT, NP> &a, bool *lost,
-                                            unsigned long long &my_conf, unsigned long long *my_edges) {
+__device__ __forceinline__ void tile_finish(const Params &P, const OffT *ro, const RoundCfg &rc, TileA<OffT, NP> &a,
+                                            bool *lost, unsigned long long &my_conf, unsigned long long *my_edges) {
     int *u = a.u;
     OffT *rb = a.rb, *re = a.re;
     const unsigned *xu = a.xu;
 #pragma unroll
     for (int j = 0; j < NP; ++j) lost[j] = false;
+    if constexpr (PHASE == 0 && FBM<F>) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+            if (u[j] < 0 || (rc.topo && (xu[j] & FB<F>))) {  // inactive (_kernels.pyx:76-77)
+                u[j] = -1;
+                continue;
+            }
+            // deg <= 16: at most 16 bits of fb0 are set, a zero bit exists
+            xput<F>(P, u[j], fb_mex_thread(P, ro, u[j], a.w0[j]));
+            if (STATS) my_edges[0] += re[j] - rb[j];
+        }
+        return;
+    }
     if (rc.topo) {
 #pragma unroll
         for (int j = 0; j < NP; ++j)
@@ -966,6 +1141,26 @@ __device__ __forceinline__ void tile_finish(const Params &P, const RoundCfg &rc,
             lost[j] = cnt != 0;
             if (!lost[j]) xput<F>(P, u[j], T | FB<F>);
         }
+        if constexpr (FBM<F>) {
+            // winners put their color into every neighbour's bitmap (once per
+            // node per solve); a lower neighbour already seen committed needs none
+#pragma unroll
+            for (int j = 0; j < NP; ++j) {
+                if (u[j] < 0 || lost[j]) continue;
+                const unsigned T = xu[j];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (nb[j][q] >= 0 && !(nb[j][q] < u[j] && (x[j][q] & FB<F>))) fb_push(P, ro, nb[j][q], T);
+                for (OffT k = rb[j] + 4; k < re[j]; k += 4) {  // deg 5..16
+                    int v2[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? colget<F>(P, k + q, u[j]) : -1;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (v2[q] >= 0) fb_push(P, ro, v2[q], T);
+                }
+            }
+        }
     }
 }
 
@@ -987,9 +1182,9 @@ __device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Sme
     unsigned seg = lo < hi ? list_segment(rc.L[bin], sm.prefix[bin], lo) : 0u;  // once per chunk
     for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG)
         group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out, out_od,
-                                          &sm.out_cnt, sm.win_bm[warp], seg, my_conf, my_edges);
+                                          &sm.out_cnt, sm.win_bm[warp], seg, my_conf, my_edges, np, bin);
     __syncthreads();
-    if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, c, sm.out_cnt);
+    if (!F::plain && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, c, sm.out_cnt);
 }
 
 // ------------------------------------------------------------------ split hubs
@@ -1150,8 +1345,8 @@ __device__ __forceinline__ void small_tile(const Params &P, const OffT *ro, cons
                                            bool *lost, unsigned long long &my_conf, unsigned long long *my_edges,
                                            unsigned &seg) {
     constexpr int NP = F::small ? NPT_SMALL : NPT;
-    tile_issue<OffT, F, NP, PHASE>(P, ro, rc, prefix, base, hi, a, seg);
-    tile_finish<OffT, F, STATS, PHASE, NP>(P, rc, a, lost, my_conf, my_edges);
+    tile_issue<OffT, F, NP, PHASE, STATS>(P, ro, rc, prefix, base, hi, a, seg);
+    tile_finish<OffT, F, STATS, PHASE, NP>(P, ro, rc, a, lost, my_conf, my_edges);
 }
 
 // A chunk of bin 0 (thread per node, NP nodes per thread per tile).
@@ -1197,10 +1392,17 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
             for (int q = 0; q < NP; ++q) {
                 u[t * NP + q] = cur.u[q];
                 lost[t * NP + q] = lt[q];
-                if constexpr (!F::small) odv[t * NP + q] = make_od(cur.rb[q], cur.re[q]);
+                if constexpr (!F::small && PHASE == 1) odv[t * NP + q] = make_od(cur.rb[q], cur.re[q]);
             }
         }
-        if (PHASE == 1) {
+        if constexpr (PHASE == 1 && F::plain) {
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+                unsigned long long odj = 0;
+                if constexpr (!F::small) odj = odv[j];
+                plain_push<F>(P, np, 0, lost[j], u[j], odj);
+            }
+        } else if (PHASE == 1) {
             unsigned bal[NS];
 #pragma unroll
             for (int j = 0; j < NS; ++j) bal[j] = __ballot_sync(FULL, lost[j]);
@@ -1229,7 +1431,7 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
             buf ^= 1u;
         }
     }
-    if (PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 0, c, written);
+    if (!F::plain && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 0, c, written);
 }
 
 // One unit of one phase.  All CTA-uniform inputs come from shared memory.
@@ -1260,7 +1462,15 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
         if (rc.topo && (xu & FB<F>)) return;  // topology sweep: inactive (_kernels.pyx:76)
         HubAcc &acc = P.hub_acc[slot];
         bool last;
-        if (PHASE == 0) {
+        if (PHASE == 0 && FBM<F>) {  // bitmap mex: no edge work to split, slice 0 assigns
+            if (slice == 0) {
+                const unsigned T = fb_mex_cta(P, ro, u, sm);
+                if (threadIdx.x == 0) {
+                    xput_t<F>(P, u, T);
+                    if (STATS) my_edges[0] += ro[u + 1] - ro[u];
+                }
+            }
+        } else if (PHASE == 0) {
             const unsigned T = assign_slice<OffT, F>(P, ro, u, slice, k, acc, sm, last);
             if (last && threadIdx.x == 0) {
                 xput_t<F>(P, u, T);
@@ -1275,6 +1485,9 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                 if (kc) dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
                 else xput<F>(P, u, xu | FB<F>);
             }
+            if constexpr (FBM<F>) {
+                if (last && kc == 0) fb_push_row_cta<OffT, F>(P, ro, u, xu);  // CTA-uniform
+            }
         }
         return;
     }
@@ -1286,7 +1499,9 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
         unsigned pushed = 0;
         if (!(rc.topo && (xu & FB<F>))) {  // topology sweep: inactive (_kernels.pyx:76)
             if (PHASE == 0) {
-                const unsigned T = assign_cta<OffT, F>(P, ro, u, sm);
+                unsigned T;
+                if constexpr (FBM<F>) T = fb_mex_cta(P, ro, u, sm);
+                else T = assign_cta<OffT, F>(P, ro, u, sm);
                 if (threadIdx.x == 0) {
                     xput_t<F>(P, u, T);
                     if (STATS) my_edges[0] += ro[u + 1] - ro[u];
@@ -1298,8 +1513,13 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                     my_conf += k;
                     if (STATS) my_edges[1] += low;
                     if (k) {
-                        if (is_hub) dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
-                        else {  // segment c, capacity 1
+                        if (is_hub) {
+                            dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
+                        } else if constexpr (F::plain) {
+                            const unsigned long long pos = atomicAdd(&P.ctrl->plain_cnt[np][3], 1ull);
+                            dyn_list(P, np, 3)[pos] = u;
+                            dyn_od(P, np, 3)[pos] = make_od(ro[u], ro[u + 1]);
+                        } else {  // segment c, capacity 1
                             dyn_list(P, np, 3)[c] = u;
                             dyn_od(P, np, 3)[c] = make_od(ro[u], ro[u + 1]);
                         }
@@ -1308,9 +1528,12 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                         xput<F>(P, u, xu | FB<F>);
                     }
                 }
+                if constexpr (FBM<F>) {
+                    if (k == 0) fb_push_row_cta<OffT, F>(P, ro, u, xu);  // CTA-uniform
+                }
             }
         }
-        if (!is_hub && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 3, c, pushed);
+        if (!F::plain && !is_hub && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 3, c, pushed);
     } else if (unit < ub[2]) {
         group_chunk<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
     } else if (unit < ub[3]) {
@@ -1353,7 +1576,10 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
     const long long gthreads = (long long)P.nblocks * BLOCK;
     RoundCfg &rc = sm.rc;
 
-    for (long long u = gtid; u < P.n; u += gthreads) xraw<F>(P, u, 0u);
+    for (long long u = gtid; u < P.n; u += gthreads) {
+        xraw<F>(P, u, 0u);
+        if constexpr (FBM<F>) P.fb0[u] = 0u;
+    }
     if (threadIdx.x == 0) {
         unsigned long long off = 0;
         for (int b = 0; b < NBIN; ++b) {
@@ -1391,7 +1617,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         const int p = (int)(t & 1), np = p ^ 1;
         // ---- current worklist sizes: rebuild the segment prefix of the
         //      previous round's output (round 1: the full static lists)
-        if (t > 1) {
+        if (!F::plain && t > 1) {
 #pragma unroll 1
             for (int b = 0; b < NSB; ++b) {
                 const unsigned ns = rc.prev_nseg[b];
@@ -1437,9 +1663,14 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                     rc.L[b] = List{rc.stat_lists[b], rc.stat_od[b], 0, 0, 0, false};
                     continue;
                 }
-                rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false}
-                                 : List{dyn_list(P, p, b), dyn_od(P, p, b), sm.prefix[F::small ? 0 : b][rc.prev_nseg[b]],
-                                        rc.prev_nseg[b], rc.prev_cap[b], true};
+                if constexpr (F::plain)  // dense, unordered lists of the previous round's pushes
+                    rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false}
+                                     : List{dyn_list(P, p, b), dyn_od(P, p, b), ld_relaxed_u64(&C->plain_cnt[p][b]), 0,
+                                            0, false};
+                else
+                    rc.L[b] = t == 1 ? List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false}
+                                     : List{dyn_list(P, p, b), dyn_od(P, p, b), sm.prefix[F::small ? 0 : b][rc.prev_nseg[b]],
+                                            rc.prev_nseg[b], rc.prev_cap[b], true};
             }
             const unsigned long long hub_total = t == 1 ? rc.nst[BIN_HUB] : ld_relaxed_u64(&C->hub_cnt[p]);
             rc.L[BIN_HUB] = List{t == 1 ? rc.stat_lists[BIN_HUB] : dyn_list(P, p, BIN_HUB), nullptr, hub_total, 0, 0,
@@ -1485,7 +1716,10 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
             rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
             rc.ubase[5] = rc.ubase[4] + (live ? rc.nch[0] : 0u);
-            sm.red = sg;  // broadcast |W_t|
+            // a tentative color overflowed the 16-bit state word: stop now (the
+            // host redoes the solve with 32-bit words), never loop on a
+            // truncated color
+            sm.red = (!F::mg && __ldcg(P.fmt_overflow)) ? 0ull : sg;  // broadcast |W_t|
             if (blockIdx.x == 0) {
                 const unsigned long long now = globaltimer();
                 if (t > 1) {  // finish the record of round t-1 (driver.py:159-168)
@@ -1502,6 +1736,8 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                     }
                     C->conflicts[q] = 0;
                     C->hub_cnt[q] = 0;
+                    if constexpr (F::plain)
+                        for (int b = 0; b < NSEG_BINS; ++b) C->plain_cnt[q][b] = 0;
                     C->wl_next[q] = 0;
                     C->unit_ctr[0][q] = C->unit_ctr[1][q] = 0;
                 }
@@ -1719,7 +1955,7 @@ inline size_t seg_capacity(long long cnt) {
 
 struct Layout {
     size_t ctrl, x, stat, dyn[2][NBIN], stat_od, dyn_od[2][NSEG_BINS], ro32, ci16, hub_acc, part, bnd, ptrs,
-        maxdeg, total;
+        maxdeg, fb0, fbx, fbx_bytes, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
@@ -1744,13 +1980,18 @@ static Layout layout(long long n, long long m, long long nown, bool mg) {
             L.dyn_od[p][b] = o;
             o = align_up(o + 8 * seg_capacity(nown), 256);
         }
-    L.ro32 = o; o = align_up(o + 4 * (size_t)(n + 1), 256);
+    L.ro32 = o; o = align_up(o + 4 * (size_t)(nown + 1), 256);
     L.ci16 = o; o = align_up(o + (m < 0x7fffffffLL ? 2 * (size_t)m : 0) + 256, 256);
     L.hub_acc = o; o = align_up(o + sizeof(HubAcc) * MAX_SPLIT_SLOTS, 256);
     L.part = o; o = align_up(o + part_scratch_bytes(NKEY, nown), 256);
     L.bnd = o; o = align_up(o + (mg ? (size_t)nown : 0), 256);
     L.ptrs = o; o = align_up(o + (mg ? 2 * sizeof(void *) * MG_MAX_WORLD + 8 * (MG_MAX_WORLD + 1) + 24 : 0), 256);
     L.maxdeg = o; o = align_up(o + 8, 256);
+    // forbidden-color bitmaps (single GPU): fb0 one word per node, fbx
+    // floor(deg/32) words per node at ro >> 5 (+ slack for the group reads)
+    L.fb0 = o; o = align_up(o + (mg ? 0 : 4 * (size_t)n), 256);
+    L.fbx_bytes = mg ? 0 : 4 * ((size_t)(m >> 5) + 64);
+    L.fbx = o; o = align_up(o + L.fbx_bytes, 256);
     L.total = o;
     return L;
 }
@@ -1771,8 +2012,12 @@ static const void *pick(bool narrow, bool x16, bool c16) {
 
 // the instantiation for (offset width, state width, column format, bin-0
 // only, stats).  int64 offsets (m >= 2^31) keep 32-bit words.
-static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats, bool small = false) {
+static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats, bool small = false,
+                                 bool plain = false) {
     if (!narrow) x16 = c16 = false;
+    if (plain)  // bench-only Plain baseline (no statistics build)
+        return small ? pick<PSF32, PSF16, PSF16D, PSF32D, false>(narrow, x16, c16)
+                     : pick<PF32, PF16, PF16D, PF32D, false>(narrow, x16, c16);
     if (small)
         return stats ? pick<SF32, SF16, SF16D, SF32D, true>(narrow, x16, c16)
                      : pick<SF32, SF16, SF16D, SF32D, false>(narrow, x16, c16);
@@ -1807,7 +2052,10 @@ static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0, g_mg_ex
 // Per-solve preprocessing shared by hc_solve and hc_mg_solve, for the owned
 // range [lo, lo + nown): fresh control block, static degree-bucketed lists,
 // int32 offsets, int16 delta columns; reads back the bucket totals, the
-// delta-column verdict and (multi-GPU) the whole graph's max degree.
+// delta-column verdict and (on request) the owned rows' max degree.
+// d_row_offsets holds the owned rows only (row r = node lo+r: the whole graph
+// on one GPU, the rank's shard on several); the kernels index it by global
+// node id through the shifted pointer ro_v = d_row_offsets - lo.
 struct Prep {
     unsigned long long tot[NKEY];
     unsigned long long *d_totals;
@@ -1817,6 +2065,7 @@ struct Prep {
 
 static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_offsets, long long n,
                    long long m, bool want_maxdeg, Prep &out, cudaStream_t st) {
+    (void)n;
     const bool narrow = m < 0x7fffffffLL && !g_force_wide;
     out.narrow = narrow;
     P.ctrl = reinterpret_cast<Ctrl *>(ws + L.ctrl);
@@ -1830,21 +2079,22 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NSEG_BINS; ++b) P.dyn_od[p][b] = reinterpret_cast<unsigned long long *>(ws + L.dyn_od[p][b]);
     P.fmt_overflow = &P.ctrl->fmt_overflow;
-    const long long *ro64 = reinterpret_cast<const long long *>(d_row_offsets);
-    P.ro = narrow ? (const void *)(ws + L.ro32) : (const void *)d_row_offsets;
+    const long long *ro_loc = reinterpret_cast<const long long *>(d_row_offsets);
+    const long long *ro_v = ro_loc - P.lo;  // indexed by global node id (owned nodes only)
+    P.ro = narrow ? (const void *)(reinterpret_cast<const int *>(ws + L.ro32) - P.lo) : (const void *)ro_v;
     // static degree-bucketed lists of the owned nodes (bins contiguous, see DegreeKey)
-    int rc = bucket_sort<NKEY>(P.nown, DegreeKey{ro64 + P.lo}, EmitI32{P.lo}, P.stat, ws + L.part,
+    int rc = bucket_sort<NKEY>(P.nown, DegreeKey{ro_loc}, EmitI32{P.lo}, P.stat, ws + L.part,
                                &out.d_totals, st);
     if (rc != HC_OK) return rc;
     const int sms = std::max(1, num_sms());
     copy_totals_kernel<<<1, 32, 0, st>>>(out.d_totals, P.ctrl);
     HC_CHECK_LAUNCH();
     if (P.nown > 0) {
-        fill_od_kernel<<<sms * 8, 256, 0, st>>>(ro64, P.stat, P.nown, P.stat_od);
+        fill_od_kernel<<<sms * 8, 256, 0, st>>>(ro_v, P.stat, P.nown, P.stat_od);
         HC_CHECK_LAUNCH();
     }
     if (narrow) {
-        narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro64, reinterpret_cast<int *>(ws + L.ro32), n + 1);
+        narrow_offsets_kernel<<<sms * 4, 256, 0, st>>>(ro_loc, reinterpret_cast<int *>(ws + L.ro32), P.nown + 1);
         HC_CHECK_LAUNCH();
     }
     // int16 delta columns of the owned rows when every |v - u| < 2^15
@@ -1852,7 +2102,7 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     HC_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
     P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
     if (narrow && m > 0 && P.nown > 0) {
-        delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro64, P.ci, P.lo, P.lo + P.nown,
+        delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro_v, P.ci, P.lo, P.lo + P.nown,
                                                       reinterpret_cast<short *>(ws + L.ci16), bad);
         HC_CHECK_LAUNCH();
     }
@@ -1860,7 +2110,7 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     out.max_degree = 0;
     if (want_maxdeg) {
         HC_CUDA_TRY(cudaMemsetAsync(d_maxdeg, 0, 8, st));
-        max_degree_kernel<<<sms * 4, 256, 0, st>>>(ro64, n, d_maxdeg);
+        max_degree_kernel<<<sms * 4, 256, 0, st>>>(ro_loc, P.nown, d_maxdeg);
         HC_CHECK_LAUNCH();
     }
     unsigned h_bad = 1;
@@ -2003,10 +2253,30 @@ int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t
                           d_colors, d_rec, max_rec, h_rounds, nullptr, d_ws, ws_bytes, stream);
 }
 
+static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                      int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec,
+                      int64_t max_rec, int64_t *h_rounds, int64_t *d_stats, void *d_ws, size_t ws_bytes,
+                      void *stream, bool plain);
+
 int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
                    int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
                    hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, int64_t *d_stats,
                    void *d_ws, size_t ws_bytes, void *stream) {
+    return solve_impl(d_row_offsets, d_col_indices, num_nodes, num_edges, mode, thr_count, d_colors, d_rec,
+                      max_rec, h_rounds, d_stats, d_ws, ws_bytes, stream, false);
+}
+
+int hc_solve_plain(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                   int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec,
+                   int64_t max_rec, int64_t *h_rounds, void *d_ws, size_t ws_bytes, void *stream) {
+    return solve_impl(d_row_offsets, d_col_indices, num_nodes, num_edges, mode, thr_count, d_colors, d_rec,
+                      max_rec, h_rounds, nullptr, d_ws, ws_bytes, stream, true);
+}
+
+static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                      int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec,
+                      int64_t max_rec, int64_t *h_rounds, int64_t *d_stats, void *d_ws, size_t ws_bytes,
+                      void *stream, bool plain) {
     HC_REQUIRE(num_nodes >= 0 && num_nodes < 0x7fffffffLL, HC_ERR_INVALID,
                "hc_solve: num_nodes %lld out of range", (long long)num_nodes);
     HC_REQUIRE(num_edges >= 0, HC_ERR_INVALID, "hc_solve: num_edges < 0");
@@ -2028,6 +2298,8 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
     P.lo = 0;
     P.nown = num_nodes;
     P.X = reinterpret_cast<unsigned *>(ws + L.x);
+    P.fb0 = reinterpret_cast<unsigned *>(ws + L.fb0);
+    P.fbx = reinterpret_cast<unsigned *>(ws + L.fbx);
     P.rec = d_rec;
     P.max_rec = d_rec ? max_rec : 0;
     P.colors_out = reinterpret_cast<long long *>(d_colors);
@@ -2060,8 +2332,9 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
             if (d_stats && P.max_rec)
                 HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
         }
+        HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
         void *args[] = {&P};
-        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr, small);
+        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr, small, plain);
         const int per_sm = occupancy_of(fn);
         HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
         P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
@@ -2089,6 +2362,7 @@ size_t hc_mg_shared_bytes(int64_t num_nodes) {
 }
 
 size_t hc_mg_workspace_bytes(int64_t num_nodes, int64_t num_edges, int64_t lo, int64_t hi) {
+    // num_edges: the shard's half-edges
     const long long n = num_nodes < 0 ? 0 : num_nodes;
     const long long nown = hi > lo ? hi - lo : 0;
     return layout(n, num_edges < 0 ? 0 : num_edges, nown, true).total;
@@ -2147,7 +2421,8 @@ int hc_mg_ipc_close(void *d_ptr, int64_t offset) {
 int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
                   int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                   int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
-                  int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
+                  int ctas, int64_t timeout_ms, int64_t global_max_degree, void *d_ws, size_t ws_bytes,
+                  void *stream) {
     HC_REQUIRE(h_bounds && world >= 1 && world <= MG_MAX_WORLD && rank >= 0 && rank < world, HC_ERR_INVALID,
                "hc_mg_solve: rank %d / world %d invalid (world <= %d)", rank, world, MG_MAX_WORLD);
     for (int q = 0; q < world; ++q)
@@ -2186,9 +2461,12 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
     P.world = world;
     P.timeout_ns = (timeout_ms > 0 ? timeout_ms : 60000) * 1000000LL;
     P.exchange = g_mg_exchange;
+    HC_REQUIRE(global_max_degree >= 0 || world == 1, HC_ERR_INVALID,
+               "hc_mg_solve: global_max_degree required when world > 1");
     Prep pr;
-    int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, true, pr, st);
+    int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, global_max_degree < 0, pr, st);
     if (rc != HC_OK) return rc;
+    if (global_max_degree >= 0) pr.max_degree = (unsigned long long)global_max_degree;
     // peer masks of the owned nodes + boundary zones
     unsigned char *bnd = reinterpret_cast<unsigned char *>(ws + L.bnd);
     long long *d_bounds = reinterpret_cast<long long *>(ws + L.ptrs + 2 * sizeof(void *) * MG_MAX_WORLD);
@@ -2199,7 +2477,7 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
     HC_CUDA_TRY(cudaMemsetAsync(d_zones, 0, 24, st));
     if (hi > lo && num_edges > 0) {
         const long long blocks = std::min<long long>((hi - lo + 7) / 8, (long long)std::max(1, num_sms()) * 16);
-        mg_boundary_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long *>(d_row_offsets),
+        mg_boundary_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const long long *>(d_row_offsets) - lo,
                                                               d_col_indices, d_bounds, world, rank, bnd, d_zones);
         HC_CHECK_LAUNCH();
     }
@@ -2258,10 +2536,11 @@ int hc_mg_launch(void *d_ws, void *stream) {
 int hc_mg_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
                 int64_t num_edges, const int64_t *h_bounds, int rank, int world, void *const *h_shared,
                 int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
-                int ctas, int64_t timeout_ms, void *d_ws, size_t ws_bytes, void *stream) {
+                int ctas, int64_t timeout_ms, int64_t global_max_degree, void *d_ws, size_t ws_bytes,
+                void *stream) {
     const int rc = hc_mg_prepare(d_row_offsets, d_col_indices, num_nodes, num_edges, h_bounds, rank, world,
-                                 h_shared, mode, thr_count, d_colors, d_rec, max_rec, ctas, timeout_ms, d_ws,
-                                 ws_bytes, stream);
+                                 h_shared, mode, thr_count, d_colors, d_rec, max_rec, ctas, timeout_ms,
+                                 global_max_degree, d_ws, ws_bytes, stream);
     return rc != HC_OK ? rc : hc_mg_launch(d_ws, stream);
 }
 

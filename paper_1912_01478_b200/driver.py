@@ -158,12 +158,14 @@ class Solver:
         self.rec = torch.empty((self.max_rec, _lib.REC_FIELDS), dtype=torch.int64,
                                device=self.g.device)
 
-    def run(self, mode: str, thr_count: int, *, fetch_records: bool = True) -> DeviceSolve:
+    def run(self, mode: str, thr_count: int, *, fetch_records: bool = True, plain: bool = False) -> DeviceSolve:
+        """plain=True: the bench-only Plain baseline (hc_solve_plain: unordered,
+        atomically pushed worklists); same results."""
         g = self.g
         rounds = ctypes.c_int64(0)
         st = torch.cuda.current_stream()
         self.start.record(st)
-        rc = self.L.hc_solve(
+        rc = (self.L.hc_solve_plain if plain else self.L.hc_solve)(
             g.row_offsets.data_ptr(), _lib.ptr(g.col_indices), g.num_nodes, g.num_edges,
             _lib.MODE_CODES[mode], int(thr_count), self.colors.data_ptr(), self.rec.data_ptr(),
             self.max_rec, ctypes.byref(rounds), self.ws.data_ptr(), self.ws.numel(),
@@ -171,7 +173,7 @@ class Solver:
         self.stop.record(st)
         if rc == _lib.HC_ERR_RECORDS:  # more rounds than record slots: grow and redo
             self._grow_records(rounds.value)
-            return self.run(mode, thr_count, fetch_records=fetch_records)
+            return self.run(mode, thr_count, fetch_records=fetch_records, plain=plain)
         _lib.check(rc)
         self.stop.synchronize()
         secs = self.start.elapsed_time(self.stop) / 1e3

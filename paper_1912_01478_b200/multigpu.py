@@ -3,7 +3,9 @@
 
 The reference has one process and one round loop (driver.py:122-176).  Here
 the node range is cut into P contiguous, edge-balanced ranges; rank p owns
-[lo_p, hi_p) and runs ONE persistent kernel for the whole solve -- the
+[lo_p, hi_p), holds only those CSR rows (a `CsrShard`: build_csr's rows
+lo_p..hi_p-1 with global column ids, built on the rank's GPU by
+hc_build_csr_rows) and runs ONE persistent kernel for the whole solve -- the
 single-GPU solver (hcb_solve.cu) instantiated with the multi-GPU format:
 
   * every rank keeps a replica of the state words X[n] in its *shared region*
@@ -37,7 +39,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .driver import HybridConfig, RoundRecord, RunReport, threshold_count
+from .driver import HybridConfig, RoundRecord, RunReport, _colors_used_device, threshold_count
 from .graph import DeviceCsr
 
 MAX_WORLD = 8
@@ -64,23 +66,135 @@ def partition_bounds_device(row_offsets: torch.Tensor, world: int) -> list[tuple
     return [(cuts[p], cuts[p + 1]) for p in range(world)]
 
 
+@dataclass
+class CsrShard:
+    """Rows [lo, hi) of the graph's CSR on this rank's GPU (SURVEY.md §8(e):
+    "each GPU holds its CSR rows"): row_offsets int64[hi-lo+1] (row r = node
+    lo+r, starting at 0), col_indices int32 with GLOBAL node ids -- exactly
+    rows lo..hi-1 of build_csr (graph.py:184-201).  num_nodes / max_degree /
+    num_undirected_edges describe the whole graph (all-reduced over ranks)."""
+
+    num_nodes: int
+    lo: int
+    hi: int
+    row_offsets: torch.Tensor
+    col_indices: torch.Tensor
+    bounds: list
+    max_degree: int = -1              # global (max over ranks); -1 until known
+    num_undirected_edges: int = -1    # global; -1 until known
+
+    @property
+    def num_edges(self) -> int:
+        """half-edges held by this shard"""
+        return int(self.col_indices.numel())
+
+    @property
+    def device(self) -> torch.device:
+        return self.row_offsets.device
+
+    def local_max_degree(self) -> int:
+        if self.hi == self.lo:
+            return 0
+        return int((self.row_offsets[1:] - self.row_offsets[:-1]).max().item())
+
+    def nbytes(self) -> int:
+        return self.row_offsets.numel() * 8 + self.col_indices.numel() * 4
+
+    def to_host(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """(row offsets, int64 column ids) in page-locked host memory -- the
+        reference's CsrGraph layout of these rows (graph.py:49-67)."""
+        ro = self.row_offsets.cpu().pin_memory()
+        ci = self.col_indices.to(torch.int64).cpu().pin_memory()
+        return ro, ci
+
+    @classmethod
+    def upload(cls, host: tuple[torch.Tensor, torch.Tensor], like: "CsrShard",
+               dev: torch.device | None = None) -> "CsrShard":
+        """Upload host rows (to_host) and narrow the column ids to int32 on the GPU."""
+        dev = dev or like.device
+        ro_h, ci_h = host
+        ro = ro_h.to(dev, non_blocking=True)
+        m = int(ci_h.numel())
+        ci = torch.empty(max(m, 1), dtype=torch.int32, device=dev)[:m]
+        if m:
+            ci64 = ci_h.to(dev, non_blocking=True)
+            _lib.check(_lib.load().hc_narrow_i64_i32(ci64.data_ptr(), ci.data_ptr(), m, _lib.stream_handle()))
+            del ci64
+        return cls(like.num_nodes, like.lo, like.hi, ro, ci, like.bounds, like.max_degree,
+                   like.num_undirected_edges)
+
+
+def shard_of(graph: DeviceCsr, bounds: list[tuple[int, int]], rank: int) -> CsrShard:
+    """Rank `rank`'s rows of a whole-graph DeviceCsr (virtual ranks on one GPU,
+    tests): a rebased copy of the offsets and a view of the columns."""
+    lo, hi = bounds[rank]
+    ro = graph.row_offsets[lo : hi + 1]
+    base = int(ro[0].item()) if hi >= lo else 0
+    end = int(ro[-1].item())
+    return CsrShard(graph.num_nodes, lo, hi, (ro - base).contiguous(), graph.col_indices[base:end], bounds,
+                    max_degree=graph.max_degree, num_undirected_edges=graph.num_undirected_edges)
+
+
+def edge_partition_bounds(d_edges: torch.Tensor, num_nodes: int, world: int) -> list[tuple[int, int]]:
+    """Edge-balanced contiguous ranges cut on the pair list's half-edge
+    counts (loops dropped, duplicates kept: hc_edge_degrees) -- every rank
+    computes the same bounds from the same generated pairs before any shard
+    exists (partition_bounds_device's rule on that prefix)."""
+    L = _lib.load()
+    n = int(num_nodes)
+    m = int(d_edges.shape[0]) if d_edges.numel() else 0
+    deg = torch.empty(max(n, 1), dtype=torch.int64, device=d_edges.device)
+    _lib.check(L.hc_edge_degrees(_lib.ptr(d_edges), m, n, deg.data_ptr(), _lib.stream_handle()))
+    ro = torch.zeros(n + 1, dtype=torch.int64, device=d_edges.device)
+    if n:
+        torch.cumsum(deg[:n], 0, out=ro[1:])
+    return partition_bounds_device(ro, world), ro
+
+
+def build_shard(d_edges: torch.Tensor, num_nodes: int, bounds: list[tuple[int, int]], rank: int,
+                raw_offsets: torch.Tensor | None = None) -> CsrShard:
+    """build_csr's rows [lo, hi) of the pair list `d_edges` (int64[m, 2] on this
+    rank's GPU), global column ids, without building any other row
+    (hc_build_csr_rows)."""
+    L = _lib.load()
+    dev = d_edges.device
+    n = int(num_nodes)
+    m = int(d_edges.shape[0]) if d_edges.numel() else 0
+    lo, hi = bounds[rank]
+    if raw_offsets is None:
+        _, raw_offsets = edge_partition_bounds(d_edges, n, len(bounds))
+    cap = int(raw_offsets[hi].item() - raw_offsets[lo].item())  # directed entries before dedupe
+    ro = torch.zeros(hi - lo + 1, dtype=torch.int64, device=dev)
+    ci = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    ws = _lib.workspace(L.hc_build_csr_rows_workspace_bytes(n, lo, hi, cap), dev)
+    md = ctypes.c_int64(0)
+    _lib.check(L.hc_build_csr_rows(_lib.ptr(d_edges), m, n, lo, hi, cap, ro.data_ptr(), ci.data_ptr(),
+                                   ctypes.byref(md), ws.data_ptr(), ws.numel(), _lib.stream_handle()))
+    del ws
+    k = int(md.value)
+    return CsrShard(n, lo, hi, ro, ci[:k].clone() if k else ci[:0], bounds)
+
+
 class RankSolver:
     """One rank's reusable solve state for the owned range [lo, hi):
     workspace, owned colors and the (global) per-round records."""
 
-    def __init__(self, graph: DeviceCsr, bounds: list[tuple[int, int]], rank: int, world: int,
+    def __init__(self, shard: CsrShard, rank: int, world: int,
                  shared_ptrs: list[int], *, max_rec: int | None = None, ctas: int = 0,
                  timeout_ms: int = 60000):
         if not 1 <= world <= MAX_WORLD:
             raise ValueError(f"world size {world} not in [1, {MAX_WORLD}]")
+        if shard.max_degree < 0:
+            raise ValueError("shard.max_degree (the global max over ranks) must be set")
         self.L = _lib.load()
-        self.g = graph
-        lo, hi = bounds[rank]
-        self.lo, self.hi, self.rank, self.world = int(lo), int(hi), int(rank), int(world)
+        self.g = shard
+        bounds = shard.bounds
+        self.lo, self.hi, self.rank, self.world = int(shard.lo), int(shard.hi), int(rank), int(world)
+        assert (self.lo, self.hi) == tuple(bounds[rank])
         self.cuts = (ctypes.c_int64 * (world + 1))(*([b[0] for b in bounds] + [bounds[-1][1]]))
-        dev = graph.device
-        n = graph.num_nodes
-        self.ws = _lib.workspace(self.L.hc_mg_workspace_bytes(n, graph.num_edges, self.lo, self.hi), dev)
+        dev = shard.device
+        n = shard.num_nodes
+        self.ws = _lib.workspace(self.L.hc_mg_workspace_bytes(n, shard.num_edges, self.lo, self.hi), dev)
         self.colors = torch.empty(max(self.hi - self.lo, 1), dtype=torch.int64, device=dev)
         self.max_rec = int(max_rec if max_rec is not None else max(1, min(n, 1 << 20)))
         self.rec = torch.empty((self.max_rec, _lib.REC_FIELDS), dtype=torch.int64, device=dev)
@@ -100,7 +214,7 @@ class RankSolver:
             ctypes.cast(self.cuts, ctypes.c_void_p), self.rank, self.world, ctypes.cast(self.shared, ctypes.c_void_p),
             _lib.MODE_CODES[mode], int(thr_count),
             self.colors.data_ptr(), self.rec.data_ptr(), self.max_rec, self.ctas, self.timeout_ms,
-            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(stream)))
+            int(g.max_degree), self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(stream)))
 
     def wait(self, stream: torch.cuda.Stream | None = None) -> int:
         rounds = ctypes.c_int64(0)
@@ -111,8 +225,8 @@ class RankSolver:
         return self.rec[:rounds].cpu().numpy()
 
 
-def _report(graph_name, dg, config, recs, rounds, seconds) -> RunReport:
-    report = RunReport(graph_name, dg.num_nodes, dg.num_undirected_edges, config)
+def _report(graph_name, num_nodes, num_undirected_edges, config, recs, rounds, seconds) -> RunReport:
+    report = RunReport(graph_name, num_nodes, num_undirected_edges, config)
     for r in recs:
         report.per_round.append(RoundRecord(
             round=int(r[0]), mode_used="topo" if r[1] else "data", worklist_size_in=int(r[2]),
@@ -155,7 +269,9 @@ class VirtualMesh:
                         for _ in range(world)]
         ptrs = [r.data_ptr() for r in self.regions]
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(world)]
-        self.ranks = [RankSolver(graph, self.bounds, p, world, ptrs, ctas=ctas, timeout_ms=timeout_ms)
+        graph = graph.ensure_lower_first()
+        self.shards = [shard_of(graph, self.bounds, p) for p in range(world)]
+        self.ranks = [RankSolver(self.shards[p], p, world, ptrs, ctas=ctas, timeout_ms=timeout_ms)
                       for p in range(world)]
         torch.cuda.synchronize()
 
@@ -193,9 +309,21 @@ def virtual_color_graph(graph: DeviceCsr, config: HybridConfig | None = None, wo
     if len(set(rounds)) != 1:
         raise RuntimeError(f"ranks disagree on the round count: {rounds}")
     recs = [rk.records(rounds[0]) for rk in mesh.ranks]
-    colors = torch.cat([rk.colors[: rk.hi - rk.lo] for rk in mesh.ranks]).cpu().numpy()
-    return MgResult(colors, _report(graph_name, graph, config, recs[0], rounds[0], secs),
-                    mesh.bounds, recs, secs)
+    dcolors = torch.cat([rk.colors[: rk.hi - rk.lo] for rk in mesh.ranks])
+    rep = _report(graph_name, graph.num_nodes, graph.num_undirected_edges, config, recs[0], rounds[0], secs)
+    rep.valid = sum(_verify_shard(sh, dcolors) for sh in mesh.shards) == 0
+    rep.colors_used = _colors_used_device(dcolors) if rep.valid else int(dcolors.max().item())
+    return MgResult(dcolors.cpu().numpy(), rep, mesh.bounds, recs, secs)
+
+
+def _verify_shard(shard: CsrShard, colors: torch.Tensor) -> int:
+    """verify_coloring (driver.py:188-204) over the shard's rows, colors global."""
+    acc = torch.zeros(1, dtype=torch.int64, device=colors.device)
+    out = ctypes.c_int64(0)
+    _lib.check(_lib.load().hc_verify_rows(shard.row_offsets.data_ptr(), _lib.ptr(shard.col_indices), shard.lo,
+                                          shard.hi, _lib.ptr(colors), acc.data_ptr(), ctypes.byref(out),
+                                          _lib.stream_handle()))
+    return int(out.value)
 
 
 # --------------------------------------------------------------------------
@@ -266,19 +394,46 @@ class PeerGroup:
 
 
 class MgSolver:
-    """Reusable per-rank multi-GPU solve of one graph (every rank holds the
-    whole CSR; each processes only its owned rows)."""
+    """Reusable per-rank multi-GPU solve of one graph.  Every rank holds only
+    its shard (CsrShard); a whole DeviceCsr is accepted too (each rank then
+    keeps only a view of its own rows: tests, single-box runs)."""
 
-    def __init__(self, graph: DeviceCsr, group=None, *, timeout_ms: int = 60000):
-        self.g = graph
-        self.peers = PeerGroup(graph.num_nodes, group)
+    def __init__(self, graph: CsrShard | DeviceCsr, group=None, *, timeout_ms: int = 60000):
+        import torch.distributed as dist
+
         self.group = group
+        if isinstance(graph, DeviceCsr):
+            world = dist.get_world_size(group)
+            graph = graph.ensure_lower_first()
+            graph = shard_of(graph, partition_bounds_device(graph.row_offsets, world), dist.get_rank(group))
+        shard = graph
+        # whole-graph facts every rank must agree on (state-word width, report)
+        if shard.max_degree < 0 or shard.num_undirected_edges < 0:
+            cdev = torch.device("cpu") if dist.get_backend(group) == "gloo" else shard.device
+            t = torch.tensor([shard.local_max_degree()], dtype=torch.int64, device=cdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+            e = torch.tensor([shard.num_edges], dtype=torch.int64, device=cdev)
+            dist.all_reduce(e, op=dist.ReduceOp.SUM, group=group)
+            shard.max_degree, shard.num_undirected_edges = int(t.item()), int(e.item()) // 2
+        self.shard = shard
+        self.peers = PeerGroup(shard.num_nodes, group)
         self.world, self.rank = self.peers.world, self.peers.rank
-        self.bounds = partition_bounds_device(graph.row_offsets, self.world)
-        self.rs = RankSolver(graph, self.bounds, self.rank, self.world, self.peers.ptrs, timeout_ms=timeout_ms)
+        if len(shard.bounds) != self.world:
+            raise ValueError(f"shard cut for {len(shard.bounds)} ranks, group has {self.world}")
+        self.bounds = shard.bounds
+        self.rs = RankSolver(shard, self.rank, self.world, self.peers.ptrs, timeout_ms=timeout_ms)
         self.mx = max(h - l for l, h in self.bounds)
         self.start = torch.cuda.Event(enable_timing=True)
         self.stop = torch.cuda.Event(enable_timing=True)
+
+    @property
+    def num_nodes(self) -> int:
+        return self.shard.num_nodes
+
+    def replace_shard(self, shard: CsrShard) -> None:
+        """Solve a freshly uploaded copy of the same rows next time (e2e bench)."""
+        shard.max_degree, shard.num_undirected_edges = self.shard.max_degree, self.shard.num_undirected_edges
+        self.shard = self.rs.g = shard
 
     def run(self, mode: str, thr_count: int) -> tuple[int, float]:
         st = torch.cuda.current_stream()
@@ -301,24 +456,42 @@ class MgSolver:
         out = out.view(self.world, -1)
         return torch.cat([out[p, : hi - lo] for p, (lo, hi) in enumerate(self.bounds)])
 
+    def verify(self, colors: torch.Tensor) -> int:
+        """Invalid edges of the whole coloring (driver.py:188-204): each rank
+        checks its rows, summed over the group."""
+        import torch.distributed as dist
+
+        bad = _verify_shard(self.shard, colors.to(self.shard.device))
+        cdev = torch.device("cpu") if dist.get_backend(self.group) == "gloo" else self.shard.device
+        t = torch.tensor([bad], dtype=torch.int64, device=cdev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return int(t.item())
+
     def close(self):
         self.peers.close()
 
 
-def mg_color_graph(graph: DeviceCsr, config: HybridConfig | None = None, *, group=None,
+def mg_color_graph(graph: CsrShard | DeviceCsr, config: HybridConfig | None = None, *, group=None,
                    graph_name: str = "graph", solver: MgSolver | None = None) -> MgResult:
     """Partitioned solve of the whole graph, one process per GPU.  Returns the
-    whole coloring and the global RunReport on every rank."""
+    whole coloring and the global RunReport (valid / colors_used included,
+    driver.py:170-176) on every rank."""
     config = config or HybridConfig()
     own = solver is None
     solver = solver or MgSolver(graph, group)
     try:
-        rounds, secs = solver.run(config.mode, threshold_count(config, graph.num_nodes))
+        n = solver.num_nodes
+        rounds, secs = solver.run(config.mode, threshold_count(config, n))
         recs = solver.rs.records(rounds)
-        colors = solver.gather_colors().cpu().numpy()
+        dcolors = solver.gather_colors()
+        bad = solver.verify(dcolors)
     finally:
         if own:
             solver.close()
-    rep = _report(graph_name, graph, config, recs, rounds, secs)
+    rep = _report(graph_name, n, solver.shard.num_undirected_edges, config, recs, rounds, secs)
+    rep.valid = bad == 0
+    colors = dcolors.cpu().numpy()
+    if colors.size and colors.min() < 1:
+        raise ValueError("invalid coloring: uncolored node (color 0) present")  # driver.py:183-184
     rep.colors_used = int(colors.max()) if colors.size else 0
     return MgResult(colors, rep, solver.bounds, [recs], secs)

@@ -350,3 +350,20 @@ def test_sorted_caller_csr_is_not_copied():
     before = dg.col_indices.data_ptr()
     dg.ensure_lower_first()
     assert dg.lower_first and dg.col_indices.data_ptr() == before
+
+
+def test_plain_baseline_same_results(corpus):
+    """hc_solve_plain (bench-only Plain baseline: unordered atomically pushed
+    worklists) computes the same colors and records as hc_solve."""
+    graphs = [G.build_csr_device(G.gen_rmat_edges(13, 16, 2), 1 << 13), G.grid_graph(200, 130),
+              G.er_graph(20000, 24, 3)]
+    graphs += [_csr(g).to_device() for g in corpus[::23] if g.n > 1]
+    for dg in graphs:
+        s = hc.Solver(dg)
+        for mode in MODES:
+            thr = hc.threshold_count(hc.HybridConfig(), dg.num_nodes)
+            a = s.run(mode, thr)
+            ca = a.colors.cpu().numpy().copy()
+            b = s.run(mode, thr, plain=True)
+            assert np.array_equal(ca, b.colors.cpu().numpy()), mode
+            assert np.array_equal(a.records[:, 1:5], b.records[:, 1:5]), mode

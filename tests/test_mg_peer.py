@@ -199,3 +199,93 @@ def test_two_processes_ipc_share_one_gpu():
         assert np.array_equal(colors, want) and np.array_equal(recs, _recs4(rep)), mode
     for a, b in zip(got[0], got[1]):
         assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+
+
+# ---------------------------------------------------------------- per-rank shards
+def test_shard_build_equals_build_csr_rows():
+    """hc_build_csr_rows: rank p's shard == rows [lo_p, hi_p) of build_csr
+    (graph.py:184-201), global column ids; the shards partition the half-edges
+    (per-rank CSR bytes ~ m_dir / P on an edge-balanced cut)."""
+    from paper_1912_01478_b200.multigpu import build_shard, edge_partition_bounds
+
+    for edges, n in ((G.gen_rmat_edges(14, 16, 3), 1 << 14), (G.gen_er_edges(5000, 40000, 9), 5000),
+                     (G.gen_grid_edges(60, 70), 4200)):
+        full = G.build_csr_device(edges, n)
+        ro, ci = full.row_offsets.cpu().numpy(), full.col_indices.cpu().numpy()
+        for world in (1, 2, 3, 8):
+            bounds, raw = edge_partition_bounds(edges, n, world)
+            assert bounds[0][0] == 0 and bounds[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(bounds, bounds[1:]))
+            total = 0
+            for p in range(world):
+                sh = build_shard(edges, n, bounds, p, raw)
+                lo, hi = bounds[p]
+                want_ro = ro[lo:hi + 1] - ro[lo]
+                assert np.array_equal(sh.row_offsets.cpu().numpy(), want_ro), (n, world, p)
+                assert np.array_equal(sh.col_indices.cpu().numpy(), ci[ro[lo]:ro[hi]]), (n, world, p)
+                total += sh.num_edges
+                if world > 1 and n > 4000:  # edge-balanced: no rank holds much more than its share
+                    assert sh.num_edges <= 1.25 * full.num_edges / world + 64, (n, world, p, sh.num_edges)
+            assert total == full.num_edges
+
+
+def _ipc_shard_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_1912_01478_b200.multigpu import MgSolver, build_shard, edge_partition_bounds, mg_color_graph
+
+        n = 1 << 10
+        edges = G.gen_rmat_edges(10, 8, 5)
+        bounds, raw = edge_partition_bounds(edges, n, world)
+        shard = build_shard(edges, n, bounds, rank, raw)
+        del edges, raw
+        solver = MgSolver(shard, timeout_ms=60000)
+        out = []
+        for mode in ("hybrid", "topo"):
+            res = mg_color_graph(shard, hc.HybridConfig(mode=mode), solver=solver)
+            out.append((mode, res.colors, _recs4(res.report), res.report.valid, res.report.colors_used,
+                        res.report.num_undirected_edges, shard.num_edges))
+        solver.close()
+        q.put((rank, out, None))
+    except Exception as exc:  # reported to the parent
+        q.put((rank, None, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_processes_sharded_csr():
+    """One process per rank, each generating the pairs, cutting the same
+    edge-balanced bounds and building ONLY its own rows; the solve, the
+    records, valid and colors_used equal the single-GPU solve of the whole graph."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in procs:
+        rank, out, err = q.get(timeout=600)
+        assert err is None, f"rank {rank}: {err}"
+        got[rank] = out
+    for p in procs:
+        p.join(timeout=60)
+    dg = G.build_csr_device(G.gen_rmat_edges(10, 8, 5), 1 << 10)
+    for mode, colors, recs, valid, used, und, _ in got[0]:
+        want, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+        assert np.array_equal(colors, want) and np.array_equal(recs, _recs4(rep)), mode
+        assert valid and used == rep.colors_used and und == dg.num_undirected_edges
+    assert got[0][0][6] + got[1][0][6] == dg.num_edges  # the shards partition the half-edges
+
+
+def test_virtual_report_valid_and_colors_used():
+    dg = G.rmat_graph(11, 16, 4)
+    res = virtual_color_graph(dg, hc.HybridConfig(), 3)
+    want, rep = hc.color_graph(dg)
+    assert res.report.valid and res.report.colors_used == rep.colors_used
