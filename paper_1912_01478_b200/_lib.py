@@ -133,7 +133,10 @@ def load():
                 "(or __graft_entry__.build()); there is no CPU fallback"
             )
         L = ctypes.CDLL(str(LIB_PATH))
+        variant = "HCB_LIB" in os.environ  # tuning builds may predate newer entry points
         for name, (res, args) in _SIGS.items():
+            if variant and not hasattr(L, name):
+                continue
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args
