@@ -128,7 +128,7 @@ int hc_wl_swap_and_sort(const int64_t *d_next, const int64_t *d_cursor, int64_t 
  * *h_rounds = total rounds.  If rounds > max_rec the solve still completes,
  * the first max_rec records are kept and HC_ERR_RECORDS is returned. */
 size_t hc_solve_workspace_bytes(int64_t num_nodes, int64_t num_edges);
-/* Storage-format overrides for tests and experiments (process-wide):
+/* Storage-format overrides for tests and experiments (per calling host thread):
  * force int64 row offsets, forbid 16-bit state words, forbid 16-bit delta
  * columns.  Defaults (0, 0, 0) let hc_solve pick per graph. */
 int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16);
@@ -222,7 +222,7 @@ int hc_mg_prepare(const int64_t *d_row_offsets, const int32_t *d_col_indices, in
                   void *stream);
 int hc_mg_launch(void *d_ws, void *stream);
 int hc_mg_wait(void *d_ws, int64_t *h_rounds, void *stream);
-/* How a rank's boundary words reach its peers (process-wide; tests /
+/* How a rank's boundary words reach its peers (per calling host thread; tests /
  * experiments): 0 = per round, the cheaper of (1) mirroring every boundary
  * store and (2) copying the boundary zones at the end of each phase. */
 int hc_mg_set_exchange(int mode);

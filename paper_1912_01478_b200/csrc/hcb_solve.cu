@@ -592,8 +592,11 @@ __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
 // of round t reads them after the grid barrier that ends round t-1: the bitmap
 // then holds exactly the colors committed before round t, i.e. the
 // reference's colors_read snapshot restricted to u's neighbours.
+#ifndef HC_FBM
+#define HC_FBM 1
+#endif
 template <class F>
-constexpr bool FBM = !F::mg;  // the multi-GPU solve keeps the adjacency-scan assign
+constexpr bool FBM = HC_FBM && !F::mg;  // the multi-GPU solve keeps the adjacency-scan assign
 
 // winner's color c into neighbour v's bitmap (fire-and-forget RED)
 template <typename OffT>
@@ -2046,8 +2049,9 @@ static int occupancy() {
 }
 
 // format overrides (tests / experiments): force int64 offsets, forbid the
-// 16-bit state word, forbid 16-bit delta columns
-static int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0, g_mg_exchange = 0;
+// 16-bit state word, forbid 16-bit delta columns, the multi-GPU exchange mode.
+// Per host thread: a knob set by one caller never changes another thread's solves.
+static thread_local int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0, g_mg_exchange = 0;
 
 // Per-solve preprocessing shared by hc_solve and hc_mg_solve, for the owned
 // range [lo, lo + nown): fresh control block, static degree-bucketed lists,
@@ -2098,7 +2102,8 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
         HC_CHECK_LAUNCH();
     }
     // int16 delta columns of the owned rows when every |v - u| < 2^15
-    unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? 2 * (size_t)m : 0));
+    // (behind the int16 columns, 16-byte aligned: a rank's shard can hold an odd number of half-edges)
+    unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? align_up(2 * (size_t)m, 16) : 0));
     HC_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
     P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
     if (narrow && m > 0 && P.nown > 0) {

@@ -37,6 +37,15 @@ if os.environ.get("HCREF_DEFAULT_CUDA") == "1":
     _ref_backend.kernels = _cuda_kernels
 
 
-def pytest_report_header(config):
+def _banner():
     return (f"refsuite_plugin: reference backends {_ref_backend.available_backends()}, "
             f"default {_ref_backend.backend_name()}")
+
+
+def pytest_report_header(config):
+    return _banner()
+
+
+def pytest_terminal_summary(terminalreporter):
+    # also under -q, where the report header is not printed
+    terminalreporter.write_line(_banner())
