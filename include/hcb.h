@@ -136,6 +136,20 @@ int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16);
  * bin-0-only instantiation (less shared memory, more resident CTAs);
  * allow = 0 forces the general kernel (tests / experiments). */
 int hc_solve_set_small(int allow);
+/* Bin-0-only graphs whose every degree is <= 4 and every |v-u| < 2^15
+ * (grids) store each row as one 8-byte word of int16 deltas (ELL4) next to
+ * the CSR and run the ELL4 instantiation; allow = 0 forces the offset +
+ * column path (per calling host thread; tests / experiments). */
+int hc_solve_set_ell(int allow);
+/* L2 residency of the state words (per calling host thread).  When the
+ * state-word array is 16 MB .. L2/3 (grids and meshes of ~8-40 M nodes)
+ * hc_solve launches the solve kernel with the array as a persisting
+ * access-policy window and sets the device's persisting set-aside
+ * (cudaLimitPersistingL2CacheSize, a device-wide limit) to exactly its
+ * size; after the solve a stream-ordered pass demotes those lines to normal
+ * (the context's other persisting lines are left alone).  allow = 0: never
+ * touch the limit or set a window. */
+int hc_solve_set_l2_window(int allow);
 int hc_solve(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
              int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors,
              hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, void *d_ws,

@@ -75,6 +75,8 @@ _SIGS = {
     "hc_solve_workspace_bytes": (ctypes.c_size_t, [_i64, _i64]),
     "hc_solve_set_formats": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "hc_solve_set_small": (ctypes.c_int, [ctypes.c_int]),
+    "hc_solve_set_l2_window": (ctypes.c_int, [ctypes.c_int]),
+    "hc_solve_set_ell": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_plain": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_stats": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, _p, ctypes.c_size_t, _p]),

@@ -280,24 +280,27 @@ def test_storage_formats_vs_oracle(leaves, extra):
 @pytest.mark.parametrize("fmt", [(1, 1, 1), (0, 1, 1), (0, 0, 1), (0, 1, 0)])
 def test_forced_storage_formats_vs_golden(configs, fmt):
     """Every (offset width, state width, column format) instantiation, with
-    and without the bin-0-only kernel, on the reference-recorded C1 graph
-    (RMAT-16) and a grid (bin-0 only)."""
+    and without the bin-0-only kernel and its ELL4 rows, on the
+    reference-recorded C1 graph (RMAT-16) and a grid (bin-0 only, degree <= 4:
+    the ELL4 kernel whenever delta columns are allowed)."""
     L = hc._lib.load()
     L.hc_solve_set_formats(*fmt)
     try:
-        for small in (1, 0):
+        for small, ell in ((1, 1), (1, 0), (0, 1)):
             L.hc_solve_set_small(small)
+            L.hc_solve_set_ell(ell)
             for key in ("rmat16", "grid64x96"):
                 kind, kw = CONFIG_SPECS[key]
                 want = configs[key]
                 dg = _device_graph(kind, kw)
                 for mode in MODES:
                     colors, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
-                    assert np.array_equal(colors, want["colors"]), (key, mode, fmt, small)
-                    assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt, small)
+                    assert np.array_equal(colors, want["colors"]), (key, mode, fmt, small, ell)
+                    assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt, small, ell)
     finally:
         L.hc_solve_set_formats(0, 0, 0)
         L.hc_solve_set_small(1)
+        L.hc_solve_set_ell(1)
 
 
 # ---------------------------------------------------------------- unsorted caller CSR
