@@ -95,6 +95,9 @@ constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 #ifndef HC_MG_PLAIN_BARRIER
 #define HC_MG_PLAIN_BARRIER 0
 #endif
+#ifndef HC_PHASE_TIMES
+#define HC_PHASE_TIMES 0
+#endif
 #ifndef HC_PAIR
 #define HC_PAIR 2   // bin-0-only kernel: tiles per loser-compaction barrier
 #endif
@@ -102,7 +105,17 @@ constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 #define HC_NPT_SMALL 2
 #endif
 constexpr int NPT_SMALL = HC_NPT_SMALL;  // the same in the bin-0-only kernel (more CTAs, fewer registers)
-static_assert(NPT_SMALL <= NPT, "shared tables are sized for NPT");
+constexpr int NPT_MAX = NPT > NPT_SMALL ? NPT : NPT_SMALL;  // sizes the shared tables
+// bitmap assign (phase 0 with forbidden-color bitmaps): nodes per thread per
+// tile.  The phase is a pure stream over the lists (entry, activity word,
+// bitmap word -> tentative word), so every bin but the hubs runs thread per
+// node and a thread keeps NPA independent nodes in flight.
+#ifndef HC_NPA
+#define HC_NPA 4
+#endif
+#ifndef HC_NPA_SMALL
+#define HC_NPA_SMALL 8
+#endif
 constexpr int NSEG_BINS = 4;             // bins 0..3 are segmented; bin 4 (hubs) is dense
 constexpr int BIN_HUB = 4;
 constexpr int NBIN = 5;
@@ -239,6 +252,7 @@ struct RoundCfg {
     unsigned long long nst[NBIN];
     unsigned csz[NSEG_BINS], nch[NSEG_BINS];
     unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
+    unsigned abase[NBIN + 1];      // bitmap-assign unit ranges (thread per node in every bin but the hubs)
     unsigned prev_nseg[NSEG_BINS], prev_cap[NSEG_BINS];
     unsigned hub_split;            // hubs split into equal-size edge slices (latency regime)
     unsigned hub_slice;            // edges per slice
@@ -256,8 +270,8 @@ struct SmemT {
     unsigned prefix[SMALL ? 1 : NSEG_BINS][MAXSEG + 1];   // segment prefix of the current lists
     unsigned win_bm[SMALL ? 1 : NW][WIN_WORDS];
     unsigned hub_bm[SMALL ? 1 : HUB_WORDS];
-    unsigned warp_tmp[NPT * NW];
-    unsigned cnt_tab[2][2 * NPT * NW];
+    unsigned warp_tmp[NPT_MAX * NW];
+    unsigned cnt_tab[2][2 * NPT_MAX * NW];
     unsigned long long red;
     int hub_first;
     unsigned unit;
@@ -1462,7 +1476,7 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     // the bin-0-only kernel compacts PAIR tiles per barrier
     constexpr int PAIR = F::small ? HC_PAIR : 1;
     constexpr int NS = PAIR * NP;  // slices per compaction
-    static_assert(NS <= 2 * NPT && NS <= 32, "cnt_tab holds 2*NPT slices, one per lane");
+    static_assert(NS <= 2 * NPT_MAX && NS <= 32, "cnt_tab holds 2*NPT_MAX slices, one per lane");
     constexpr unsigned long long STEP = (unsigned long long)BLOCK * NP;
     for (unsigned long long base = lo; base < hi; base += STEP * PAIR) {
         int u[NS];
@@ -1637,17 +1651,71 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
     }
 }
 
+// One bitmap-assign unit (phase 0 with forbidden-color bitmaps, rc.abase):
+// a hub (the CTA takes the mex of its bitmap) or BLOCK * NPA consecutive
+// entries of one bin's list, thread per node: list entry -> (activity word,
+// bitmap word fb0) -> tentative word.  No row offsets, no columns (a node whose
+// colors 1..32 are all taken reads its fbx words, fb_mex_thread).
+template <typename OffT, class F, class SMT>
+__device__ __forceinline__ void assign_unit(const Params &P, const OffT *ro, SMT &sm, unsigned unit) {
+    const RoundCfg &rc = sm.rc;
+    const unsigned *ab = rc.abase;
+    const bool topo = rc.topo;
+    if (unit < ab[1]) {  // hub (CTA-uniform)
+        if constexpr (!F::small) {
+            const int u = rc.L[BIN_HUB].base[unit];
+            if (topo && (xget<F>(P, u) & FB<F>)) return;  // inactive (_kernels.pyx:76)
+            const unsigned T = fb_mex_cta(P, ro, u, sm);
+            if (threadIdx.x == 0) xput_t<F>(P, u, T);
+        }
+        return;
+    }
+    int b = 3;
+    while (unit >= ab[5 - b]) --b;  // bins 3, 2, 1, 0 in unit order
+    constexpr int NA = F::small ? HC_NPA_SMALL : HC_NPA;
+    constexpr unsigned long long ACH = (unsigned long long)BLOCK * NA;
+    const List &L = rc.L[b];
+    const unsigned *prefix = sm.prefix[F::small ? 0 : b];
+    const unsigned long long lo = (unsigned long long)(unit - ab[4 - b]) * ACH;
+    const unsigned long long hi = min(lo + ACH, L.total);
+    const bool ident = b == 0 && rc.ident;
+    unsigned seg = (ident || lo >= hi) ? 0u : list_segment(L, prefix, lo);
+    int u[NA];
+    unsigned xu[NA], w0[NA];
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        const unsigned long long v = lo + (unsigned long long)j * BLOCK + threadIdx.x;
+        u[j] = v < hi ? (ident ? (int)(P.lo + (long long)v) : ld_entry(L.base + list_index_walk(L, prefix, v, seg)))
+                      : -1;
+    }
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        xu[j] = (topo && u[j] >= 0) ? xget<F>(P, u[j]) : 0u;
+        w0[j] = u[j] >= 0 ? P.fb0[u[j]] : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < NA; ++j) {
+        if (u[j] < 0 || (topo && (xu[j] & FB<F>))) continue;  // inactive (_kernels.pyx:76-77)
+        xput_t<F>(P, u[j], fb_mex_thread(P, ro, u[j], w0[j]));
+    }
+}
+
 template <typename OffT, class F, bool STATS, int PHASE, class SMT>
 __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, SMT &sm, int p,
                                           unsigned long long &my_conf, unsigned long long *my_edges) {
+    // bitmap assign: its own unit space (no output lists; STATS builds keep
+    // the binned path, which also counts the assign edges)
+    constexpr bool FA = PHASE == 0 && FBM<F> && !STATS;
     unsigned *ctr = &P.ctrl->unit_ctr[PHASE][p];
     if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);
     __syncthreads();
     unsigned unit = sm.unit;
+    const unsigned nunits = FA ? sm.rc.abase[NBIN] : sm.rc.ubase[NBIN];
     __syncthreads();
-    while (unit < sm.rc.ubase[NBIN]) {
+    while (unit < nunits) {
         if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);  // prefetch the next unit
-        run_unit<OffT, F, STATS, PHASE>(P, ro, sm, unit, p, my_conf, my_edges);
+        if constexpr (FA) assign_unit<OffT, F>(P, ro, sm, unit);
+        else run_unit<OffT, F, STATS, PHASE>(P, ro, sm, unit, p, my_conf, my_edges);
         __syncthreads();
         unit = sm.unit;
         __syncthreads();
@@ -1807,6 +1875,13 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
             rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
             rc.ubase[5] = rc.ubase[4] + (live ? rc.nch[0] : 0u);
+            {  // bitmap-assign units: one per hub, then BLOCK * NPA nodes per chunk of bins 3..0
+                constexpr unsigned ACH = BLOCK * (F::small ? HC_NPA_SMALL : HC_NPA);
+                rc.abase[0] = 0;
+                rc.abase[1] = live ? H : 0u;
+                for (int b = 3; b >= 0; --b)
+                    rc.abase[5 - b] = rc.abase[4 - b] + (live ? (unsigned)((rc.L[b].total + ACH - 1) / ACH) : 0u);
+            }
             // a tentative color overflowed the 16-bit state word: stop now (the
             // host redoes the solve with 32-bit words), never loop on a
             // truncated color
@@ -1833,6 +1908,9 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                     C->unit_ctr[0][q] = C->unit_ctr[1][q] = 0;
                 }
                 t_start = now;
+#if HC_PHASE_TIMES
+                if (STATS && t <= P.max_rec) P.stats[2 * P.max_rec + 3 * (t - 1)] = (long long)now;
+#endif
                 wl_in_prev = (long long)sg;
                 topo_prev = topo;
             }
@@ -1881,6 +1959,12 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         } else {
             grid_sync(&C->bar, P.nblocks);
         }
+#if HC_PHASE_TIMES
+        // development builds: per round (start, assign end, resolve end) in
+        // globaltimer ns, behind the 2 * max_rec edge counters
+        if (STATS && blockIdx.x == 0 && threadIdx.x == 0 && t <= P.max_rec)
+            P.stats[2 * P.max_rec + 3 * (t - 1) + 1] = (long long)globaltimer();
+#endif
         run_phase<OffT, F, STATS, 1>(P, ro, sm, p, my_conf, my_edges);
 
         // conflicts of this round: block reduce then one atomic per CTA
@@ -1919,6 +2003,10 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         } else {
             grid_sync(&C->bar, P.nblocks);
         }
+#if HC_PHASE_TIMES
+        if (STATS && blockIdx.x == 0 && threadIdx.x == 0 && t <= P.max_rec)
+            P.stats[2 * P.max_rec + 3 * (t - 1) + 2] = (long long)globaltimer();
+#endif
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->rounds = t - 1;
