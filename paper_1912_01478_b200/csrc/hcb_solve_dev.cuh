@@ -179,7 +179,16 @@ struct Mbox {
 
 // per-hub merge slot for hubs split across several CTAs (latency regime)
 constexpr int HA_WORDS = 62;                   // colors 65..2048 beyond the 64-bit mask
-constexpr int MAX_SPLIT_SLOTS = 1024;
+#ifndef HC_UPC3
+#define HC_UPC3 64   // bin-3 work units per CTA (at least one warp tile each)
+#endif
+#ifndef HC_MAX_SPLIT
+#define HC_MAX_SPLIT 1024
+#endif
+#ifndef HC_SPLIT_ANY
+#define HC_SPLIT_ANY 0   // split the active hubs whenever they fit the slots (not only when fewer than the CTAs)
+#endif
+constexpr int MAX_SPLIT_SLOTS = HC_MAX_SPLIT;
 struct HubAcc {
     unsigned long long mask;                   // colors 1..64 seen (assign)
     unsigned words[HA_WORDS];                  // colors 65..2048 seen (assign)
@@ -250,7 +259,8 @@ struct RoundCfg {
     const int *stat_lists[NBIN];
     const unsigned long long *stat_od[NBIN];
     unsigned long long nst[NBIN];
-    unsigned csz[NSEG_BINS], nch[NSEG_BINS];
+    unsigned csz[NSEG_BINS], nch[NSEG_BINS];  // output segment size / count per bin
+    unsigned su[NSEG_BINS], nsu[NSEG_BINS];   // work-unit size / count of the group bins 1..3
     unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
     unsigned abase[NBIN + 1];      // bitmap-assign unit ranges (thread per node in every bin but the hubs)
     unsigned prev_nseg[NSEG_BINS], prev_cap[NSEG_BINS];
@@ -258,6 +268,7 @@ struct RoundCfg {
     unsigned hub_slice;            // edges per slice
     bool topo, ident, bin3_by_cta, ident_small;
     bool bulk;                     // multi-GPU: this round's words go to the peers by zone copies
+    long long round;               // current round t (development timing builds)
 };
 
 // SMALL: the graph has only bin-0 nodes (max degree <= 16: grids, meshes,
@@ -714,10 +725,26 @@ __device__ unsigned fb_mex_cta(const Params &P, const OffT *ro, int u, SMT &sm) 
 }
 
 // a winner of the CTA-granularity paths pushes its color into every neighbour
+// (PU column loads per thread in flight, then their state words, then the
+// REDs: a hub's whole row is one pass of deg / (PU * BLOCK) round trips)
+constexpr int PU = 8;
 template <typename OffT, class F>
 __device__ __forceinline__ void fb_push_row_cta(const Params &P, const OffT *ro, int u, unsigned c) {
     const long long b = ro[u], e = ro[u + 1];
-    for (long long k = b + threadIdx.x; k < e; k += BLOCK) fb_push<F>(P, ro, colget<F, true>(P, k, u), c);
+    for (long long k0 = b + threadIdx.x; k0 < e; k0 += (long long)PU * BLOCK) {
+        int v[PU];
+        unsigned x[PU];
+#pragma unroll
+        for (int q = 0; q < PU; ++q) {
+            const long long k = k0 + (long long)q * BLOCK;
+            v[q] = k < e ? colget<F, true>(P, k, u) : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < PU; ++q) x[q] = v[q] >= 0 ? xget<F>(P, v[q]) : FB<F>;
+#pragma unroll
+        for (int q = 0; q < PU; ++q)
+            if (!(x[q] & FB<F>)) fb_push<F, false>(P, ro, v[q], c);  // committed neighbours need none
+    }
 }
 
 // ------------------------------------------------------------------ groups
@@ -908,9 +935,11 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
             if (STATS) my_edges[1] += low;
             if (cnt) {
                 if constexpr (!F::plain) {
-                    const unsigned pos = atomicAdd(out_cnt, 1u);
+                    const unsigned pos = atomicAdd(out_cnt, 1u);  // the segment's global loser count
                     out[pos] = u;
                     out_od[pos] = od;
+                    // multi-GPU: a global segment count (group_sub) bypasses seg_put's tally
+                    if (F::mg && !__isShared(out_cnt)) atomicAdd(&s_wl_acc, 1ull);
                 }
             } else {
                 xput<F>(P, u, xu | FB<F>);
@@ -923,8 +952,21 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
                         if (nb[q] != 0x7fffffff) fb_push<F>(P, ro, nb[q], xu);
-                } else {
-                    for (long long k = b + sub; k < e; k += G) fb_push<F>(P, ro, colget<F>(P, k, u), xu);
+                } else {  // whole warp, one node: PU column loads per lane in flight
+                    for (long long k0 = b + sub; k0 < e; k0 += (long long)PU * G) {
+                        int w[PU];
+                        unsigned xw[PU];
+#pragma unroll
+                        for (int q = 0; q < PU; ++q) {
+                            const long long k = k0 + (long long)q * G;
+                            w[q] = k < e ? colget<F>(P, k, u) : -1;
+                        }
+#pragma unroll
+                        for (int q = 0; q < PU; ++q) xw[q] = w[q] >= 0 ? xget<F>(P, w[q]) : FB<F>;
+#pragma unroll
+                        for (int q = 0; q < PU; ++q)
+                            if (!(xw[q] & FB<F>)) fb_push<F, false>(P, ro, w[q], xu);
+                    }
                 }
             }
         }
@@ -1270,26 +1312,43 @@ __device__ __forceinline__ void tile_finish(const Params &P, const OffT *ro, con
 }
 
 // a chunk of a group bin: warps take warp tiles of 32/G nodes round-robin
+// A unit of a group bin: rc.su[bin] consecutive list positions (whole warp
+// tiles of 32/G nodes, G lanes per node), warps take tiles round-robin.
+// Units are smaller than the output segments (rc.csz, at most MAXSEG per
+// bin), so the heaviest nodes of a round do not queue behind each other in
+// one long chunk (RMAT-22: the longest bin-3 chunk took 100-345 us of a
+// 120-410 us resolve phase); a loser goes to the segment of its position
+// through the segment's global count (zeroed at the start of the round).
 template <int G, typename OffT, class F, bool STATS, int PHASE>
-__device__ __forceinline__ void group_chunk(const Params &P, const OffT *ro, Smem &sm, int bin,
-                                            unsigned c, int np, unsigned long long &my_conf,
-                                            unsigned long long *my_edges) {
+__device__ __forceinline__ void group_sub(const Params &P, const OffT *ro, Smem &sm, int bin,
+                                          unsigned i, int np, unsigned long long &my_conf,
+                                          unsigned long long *my_edges) {
     const RoundCfg &rc = sm.rc;
     const unsigned warp = threadIdx.x >> 5;
     const unsigned csz = rc.csz[bin];
-    const unsigned long long lo = (unsigned long long)c * csz;
-    const unsigned long long hi = min(lo + csz, rc.L[bin].total);
-    int *out = dyn_list(P, np, bin) + (long long)c * csz;
-    unsigned long long *out_od = dyn_od(P, np, bin) + (long long)c * csz;
-    if (threadIdx.x == 0) sm.out_cnt = 0;
-    __syncthreads();
+    const unsigned long long lo = (unsigned long long)i * rc.su[bin];
+    const unsigned long long hi = min(lo + rc.su[bin], rc.L[bin].total);
     constexpr unsigned NG = 32 / G;
-    unsigned seg = lo < hi ? list_segment(rc.L[bin], sm.prefix[bin], lo) : 0u;  // once per chunk
-    for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG)
-        group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, out, out_od,
-                                          &sm.out_cnt, sm.win_bm[warp], seg, my_conf, my_edges, np, bin);
-    __syncthreads();
-    if (!F::plain && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, c, sm.out_cnt);
+    // unit == segment (bins 1, 2; bin 3 with few nodes): the CTA counts its
+    // losers in shared memory and writes the segment's count once
+    const bool whole = rc.su[bin] == csz;
+    if (whole) {
+        if (threadIdx.x == 0) sm.out_cnt = 0;
+        __syncthreads();
+    }
+    unsigned seg = lo < hi ? list_segment(rc.L[bin], sm.prefix[bin], lo) : 0u;  // once per unit
+    for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG) {
+        const unsigned c = (unsigned)(v0 / csz);  // a warp tile never straddles segments (csz: whole tiles)
+        group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo,
+                                          dyn_list(P, np, bin) + (long long)c * csz,
+                                          dyn_od(P, np, bin) + (long long)c * csz,
+                                          whole ? &sm.out_cnt : &P.ctrl->segcnt[np][bin][c],
+                                          sm.win_bm[warp], seg, my_conf, my_edges, np, bin);
+    }
+    if (whole) {
+        __syncthreads();
+        if (!F::plain && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, bin, i, sm.out_cnt);
+    }
 }
 
 // ------------------------------------------------------------------ split hubs
@@ -1640,11 +1699,11 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
         }
         if (!F::plain && !is_hub && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 3, c, pushed);
     } else if (unit < ub[2]) {
-        group_chunk<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
+        group_sub<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
     } else if (unit < ub[3]) {
-        group_chunk<16, OffT, F, STATS, PHASE>(P, ro, sm, 2, unit - ub[2], np, my_conf, my_edges);
+        group_sub<16, OffT, F, STATS, PHASE>(P, ro, sm, 2, unit - ub[2], np, my_conf, my_edges);
     } else if (unit < ub[4]) {
-        group_chunk<8, OffT, F, STATS, PHASE>(P, ro, sm, 1, unit - ub[3], np, my_conf, my_edges);
+        group_sub<8, OffT, F, STATS, PHASE>(P, ro, sm, 1, unit - ub[3], np, my_conf, my_edges);
     } else {
         bin0_chunk<OffT, F, STATS, PHASE>(P, ro, sm, unit - ub[4], np, my_conf, my_edges);
     }
@@ -1712,14 +1771,36 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, SMT &
     unsigned unit = sm.unit;
     const unsigned nunits = FA ? sm.rc.abase[NBIN] : sm.rc.ubase[NBIN];
     __syncthreads();
+#if HC_PHASE_TIMES
+    unsigned long long busy = 0;
+    const long long t_round = STATS ? (long long)sm.rc.round : 0;
+#endif
     while (unit < nunits) {
         if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);  // prefetch the next unit
+#if HC_PHASE_TIMES
+        const unsigned long long t0 = globaltimer();
+#endif
         if constexpr (FA) assign_unit<OffT, F>(P, ro, sm, unit);
         else run_unit<OffT, F, STATS, PHASE>(P, ro, sm, unit, p, my_conf, my_edges);
         __syncthreads();
+#if HC_PHASE_TIMES
+        // development builds, resolve: longest unit per kind (hub, bin 3..0)
+        // and the busiest CTA, per round, behind the (start, assign, resolve) times
+        if (STATS && PHASE == 1 && threadIdx.x == 0 && t_round >= 1 && t_round <= P.max_rec) {
+            const unsigned long long d = globaltimer() - t0;
+            busy += d;
+            int kind = 0;
+            while (kind < NBIN - 1 && unit >= sm.rc.ubase[kind + 1]) ++kind;
+            atomicMax((unsigned long long *)&P.stats[5 * P.max_rec + 8 * (t_round - 1) + kind], d);
+        }
+#endif
         unit = sm.unit;
         __syncthreads();
     }
+#if HC_PHASE_TIMES
+    if (STATS && PHASE == 1 && threadIdx.x == 0 && t_round >= 1 && t_round <= P.max_rec)
+        atomicMax((unsigned long long *)&P.stats[5 * P.max_rec + 8 * (t_round - 1) + 5], busy);
+#endif
 }
 
 // ------------------------------------------------------------------ kernel
@@ -1845,6 +1926,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                 for (int b = 0; b < NBIN; ++b)
                     rc.L[b] = List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false};
             rc.topo = topo;
+            rc.round = t;
             rc.ident = topo && rc.ident_small;
             if constexpr (F::mg) {
                 // bulk when copying the zones (plus the extra local barrier it
@@ -1864,16 +1946,28 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             for (int b = 0; b < NSEG_BINS; ++b)
                 rc.nch[b] = (unsigned)((rc.L[b].total + rc.csz[b] - 1) / rc.csz[b]);
             rc.bin3_by_cta = rc.csz[3] == 1u;
+            // group-bin work units: whole warp tiles, about UPC per CTA at most;
+            // bin 3 (degrees 65..4096) keeps one tile per unit up to 64 per CTA
+            for (int b = 1; b < NSEG_BINS; ++b) {
+                // bins 1, 2 (similar degrees): unit = segment; bin 3 (65..4096):
+                // about HC_UPC3 units per CTA, at least one warp tile each
+                const unsigned tile = NW * (b == 1 ? 4u : b == 2 ? 2u : 1u);
+                const unsigned long long tiles = (rc.L[b].total + tile - 1) / tile;
+                unsigned long long k = b == 3 ? tiles / ((unsigned long long)HC_UPC3 * P.nblocks) : ~0ull;
+                k = max(1ull, min(k, (unsigned long long)(rc.csz[b] / tile)));
+                rc.su[b] = (b == 3 && rc.bin3_by_cta) ? 1u : (unsigned)(k * tile);
+                rc.nsu[b] = (unsigned)((rc.L[b].total + rc.su[b] - 1) / rc.su[b]);
+            }
             const bool live = s != 0;
             rc.ubase[0] = 0;
             // few active hubs (< nblocks): split them into edge slices; the
             // slice prefix is built below by the whole CTA
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
-            rc.hub_split = (live && H > 0 && H < P.nblocks && H <= MAX_SPLIT_SLOTS) ? 1u : 0u;
+            rc.hub_split = (live && H > 0 && (HC_SPLIT_ANY || H < P.nblocks) && H <= MAX_SPLIT_SLOTS) ? 1u : 0u;
             rc.ubase[1] = live ? H : 0u;
-            rc.ubase[2] = rc.ubase[1] + (live ? rc.nch[3] : 0u);
-            rc.ubase[3] = rc.ubase[2] + (live ? rc.nch[2] : 0u);
-            rc.ubase[4] = rc.ubase[3] + (live ? rc.nch[1] : 0u);
+            rc.ubase[2] = rc.ubase[1] + (live ? rc.nsu[3] : 0u);
+            rc.ubase[3] = rc.ubase[2] + (live ? rc.nsu[2] : 0u);
+            rc.ubase[4] = rc.ubase[3] + (live ? rc.nsu[1] : 0u);
             rc.ubase[5] = rc.ubase[4] + (live ? rc.nch[0] : 0u);
             {  // bitmap-assign units: one per hub, then BLOCK * NPA nodes per chunk of bins 3..0
                 constexpr unsigned ACH = BLOCK * (F::small ? HC_NPA_SMALL : HC_NPA);
@@ -1920,6 +2014,14 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         __syncthreads();
         if (s == 0) break;  // worklist drained (driver.py:145)
         if (F::mg && blockIdx.x == 0 && threadIdx.x == 0) C->rounds = t;  // progress (timeout report)
+        if constexpr (!F::small && !F::plain) {
+            // the group bins' output segments collect their losers with global
+            // counts (group_sub): zero this round's (parity np; their last
+            // reader was the prefix rebuild of round t-1, the resolve that
+            // fills them is behind the next grid barrier)
+            for (int b = 1; b < NSEG_BINS; ++b)
+                for (long long i = gtid; i < (long long)rc.nch[b]; i += gthreads) C->segcnt[np][b][i] = 0u;
+        }
         if (!F::small && rc.hub_split) {  // CTA-uniform: equal-size edge slices over the active hubs
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
             unsigned long long e_loc = 0;
