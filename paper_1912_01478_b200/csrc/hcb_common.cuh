@@ -120,9 +120,27 @@ struct GridBarrier {
     unsigned gen;
 };
 
+#ifndef HC_FAST_BARRIER
+#define HC_FAST_BARRIER 1
+#endif
 __device__ __forceinline__ void grid_sync(GridBarrier *b, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
+#if HC_FAST_BARRIER
+        // arrival is one acq_rel atomic (releases the CTA's writes, ordered
+        // before it by the CTA barrier); the last arriver resets the count and
+        // publishes the next generation with a release store; the waiters'
+        // acquire load of it orders (and L1-invalidates) what follows
+        const unsigned g = *(volatile unsigned *)&b->gen;
+        unsigned arrived;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(arrived) : "l"(&b->count) : "memory");
+        if (arrived == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&b->count), "r"(0u) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&b->gen), "r"(g + 1u) : "memory");
+        } else {
+            while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
+        }
+#else
         unsigned g = ld_acquire_u32(&b->gen);
         __threadfence();
         unsigned arrived = atomicAdd(&b->count, 1u);
@@ -134,6 +152,7 @@ __device__ __forceinline__ void grid_sync(GridBarrier *b, unsigned nblocks) {
             while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
         }
         __threadfence();
+#endif
     }
     __syncthreads();
 }
