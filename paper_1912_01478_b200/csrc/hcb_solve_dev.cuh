@@ -185,6 +185,9 @@ constexpr int HA_WORDS = 62;                   // colors 65..2048 beyond the 64-
 #ifndef HC_UPC3
 #define HC_UPC3 16   // bin-3 work units per CTA (at least one warp tile each)
 #endif
+#ifndef HC_K3
+#define HC_K3 25   // leading bin-3 nodes taken CTA per node, in percent of the CTAs
+#endif
 #ifndef HC_MAX_SPLIT
 #define HC_MAX_SPLIT 1024
 #endif
@@ -264,6 +267,7 @@ struct RoundCfg {
     unsigned long long nst[NBIN];
     unsigned csz[NSEG_BINS], nch[NSEG_BINS];  // output segment size / count per bin
     unsigned su[NSEG_BINS], nsu[NSEG_BINS];   // work-unit size / count of the group bins 1..3
+    unsigned k3;                              // leading bin-3 positions processed CTA per node
     unsigned ubase[NBIN + 1];      // unit ranges: hub, bin3, bin2, bin1, bin0
     unsigned abase[NBIN + 1];      // bitmap-assign unit ranges (thread per node in every bin but the hubs)
     unsigned prev_nseg[NSEG_BINS], prev_cap[NSEG_BINS];
@@ -1329,12 +1333,15 @@ __device__ __forceinline__ void group_sub(const Params &P, const OffT *ro, Smem 
     const RoundCfg &rc = sm.rc;
     const unsigned warp = threadIdx.x >> 5;
     const unsigned csz = rc.csz[bin];
-    const unsigned long long lo = (unsigned long long)i * rc.su[bin];
+    // bin 3: the first k3 positions went to CTA-per-node units
+    const unsigned long long off = bin == 3 ? rc.k3 : 0u;
+    const unsigned long long lo = off + (unsigned long long)i * rc.su[bin];
     const unsigned long long hi = min(lo + rc.su[bin], rc.L[bin].total);
     constexpr unsigned NG = 32 / G;
-    // unit == segment (bins 1, 2; bin 3 with few nodes): the CTA counts its
-    // losers in shared memory and writes the segment's count once
-    const bool whole = rc.su[bin] == csz;
+    // unit == segment (bins 1, 2): the CTA counts its losers in shared
+    // memory and writes the segment's count once (bin 3: global counts; its
+    // warp tiles are single nodes, so none straddles a segment)
+    const bool whole = bin != 3 && rc.su[bin] == csz;
     if (whole) {
         if (threadIdx.x == 0) sm.out_cnt = 0;
         __syncthreads();
@@ -1688,8 +1695,10 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
         }
         return;
     }
-    if (is_hub || (rc.bin3_by_cta && unit < ub[2])) {
-        // ---- hub (or bin-3 node in the latency regime): one CTA per node
+    if (is_hub || unit < ub[1] + rc.k3) {
+        // ---- hub, or one of the first k3 bin-3 nodes (the heaviest: the
+        //      lists run in descending degree buckets), or every bin-3 node
+        //      in the latency regime: one CTA per node
         const unsigned c = is_hub ? unit : unit - ub[1];
         const int u = is_hub ? rc.L[BIN_HUB].base[c] : rc.L[3].base[list_index(rc.L[3], sm.prefix[3], c)];
         const unsigned xu = xget<F>(P, u);
@@ -1716,9 +1725,15 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                             const unsigned long long pos = atomicAdd(&P.ctrl->plain_cnt[np][3], 1ull);
                             dyn_list(P, np, 3)[pos] = u;
                             dyn_od(P, np, 3)[pos] = make_od(ro[u], ro[u + 1]);
-                        } else {  // segment c, capacity 1
+                        } else if (rc.bin3_by_cta) {  // segment c, capacity 1
                             dyn_list(P, np, 3)[c] = u;
                             dyn_od(P, np, 3)[c] = make_od(ro[u], ro[u + 1]);
+                        } else {  // the segment of position c, through its global count
+                            const unsigned sgm = c / rc.csz[3];
+                            const long long at = (long long)sgm * rc.csz[3] + atomicAdd(&P.ctrl->segcnt[np][3][sgm], 1u);
+                            dyn_list(P, np, 3)[at] = u;
+                            dyn_od(P, np, 3)[at] = make_od(ro[u], ro[u + 1]);
+                            if constexpr (F::mg) s_wl_acc += 1ull;
                         }
                         pushed = 1;
                     } else {
@@ -1730,9 +1745,9 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                 }
             }
         }
-        if (!F::plain && !is_hub && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 3, c, pushed);
+        if (!F::plain && !is_hub && rc.bin3_by_cta && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 3, c, pushed);
     } else if (unit < ub[2]) {
-        group_sub<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1], np, my_conf, my_edges);
+        group_sub<32, OffT, F, STATS, PHASE>(P, ro, sm, 3, unit - ub[1] - rc.k3, np, my_conf, my_edges);
     } else if (unit < ub[3]) {
         group_sub<16, OffT, F, STATS, PHASE>(P, ro, sm, 2, unit - ub[2], np, my_conf, my_edges);
     } else if (unit < ub[4]) {
@@ -1991,6 +2006,14 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                 rc.su[b] = (b == 3 && rc.bin3_by_cta) ? 1u : (unsigned)(k * tile);
                 rc.nsu[b] = (unsigned)((rc.L[b].total + rc.su[b] - 1) / rc.su[b]);
             }
+            // the heaviest bin-3 nodes (list front) one CTA each: a single
+            // degree-4096 node would hold a warp ~28 us (RMAT-16 resolve)
+            rc.k3 = rc.bin3_by_cta ? (unsigned)rc.L[3].total
+                                   : (unsigned)min(rc.L[3].total, (unsigned long long)(P.nblocks * HC_K3 / 100));
+            if (!rc.bin3_by_cta)
+                rc.nsu[3] = (unsigned)((rc.L[3].total - rc.k3 + rc.su[3] - 1) / rc.su[3]);
+            else
+                rc.nsu[3] = 0;
             const bool live = s != 0;
             rc.ubase[0] = 0;
             // few active hubs (< nblocks): split them into edge slices; the
@@ -1998,7 +2021,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
             rc.hub_split = (live && H > 0 && (HC_SPLIT_ANY || H < P.nblocks) && H <= MAX_SPLIT_SLOTS) ? 1u : 0u;
             rc.ubase[1] = live ? H : 0u;
-            rc.ubase[2] = rc.ubase[1] + (live ? rc.nsu[3] : 0u);
+            rc.ubase[2] = rc.ubase[1] + (live ? rc.k3 + rc.nsu[3] : 0u);
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nsu[2] : 0u);
             rc.ubase[4] = rc.ubase[3] + (live ? rc.nsu[1] : 0u);
             rc.ubase[5] = rc.ubase[4] + (live ? rc.nch[0] : 0u);
