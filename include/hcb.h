@@ -40,6 +40,7 @@ extern "C" {
 #define HC_ERR_DUPLICATE (-6)    /* duplicate push in one iteration: worklist.py:85-88  */
 #define HC_ERR_RECORDS (-7)      /* per-round record buffer too small (rounds returned) */
 #define HC_ERR_TIMEOUT (-8)      /* multi-GPU: a peer missed a cross-GPU barrier       */
+#define HC_ERR_STALLED (-9)      /* solve exceeded n rounds (broken invariant; a bug)   */
 
 #define HC_MODE_DATA 0   /* driver.py:149-150 */
 #define HC_MODE_TOPO 1   /* driver.py:147-148 */
@@ -141,6 +142,10 @@ int hc_solve_set_small(int allow);
  * the CSR and run the ELL4 instantiation; allow = 0 forces the offset +
  * column path (per calling host thread; tests / experiments). */
 int hc_solve_set_ell(int allow);
+/* Live lower lists (resolve keeps each node's still-uncolored lower
+ * neighbours, compacted in place): mode -1 = per graph (hubs present and
+ * >= 2^25 half-edges), 0 = off, 1 = on (per calling host thread). */
+int hc_solve_set_live(int mode);
 /* L2 residency of the state words (per calling host thread).  When the
  * state-word array is 16 MB .. L2/3 (grids and meshes of ~8-40 M nodes)
  * hc_solve launches the solve kernel with the array as a persisting

@@ -27,6 +27,7 @@ HC_ERR_UNCOLORED = -5
 HC_ERR_DUPLICATE = -6
 HC_ERR_RECORDS = -7
 HC_ERR_TIMEOUT = -8
+HC_ERR_STALLED = -9
 
 MODE_CODES = {"data": 0, "topo": 1, "hybrid": 2}
 
@@ -77,6 +78,7 @@ _SIGS = {
     "hc_solve_set_small": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve_set_l2_window": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve_set_ell": (ctypes.c_int, [ctypes.c_int]),
+    "hc_solve_set_live": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_plain": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_stats": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, _p, ctypes.c_size_t, _p]),

@@ -164,7 +164,7 @@ inline size_t seg_capacity(long long cnt) {
 
 struct Layout {
     size_t ctrl, x, stat, dyn[2][NBIN], stat_od, dyn_od[2][NSEG_BINS], ro32, ci16, hub_acc, part, bnd, ptrs,
-        maxdeg, fb0, fbx, fbx_bytes, ell, total;
+        maxdeg, fb0, fbx, fbx_bytes, ell, lc, lcnt, total;
 };
 
 // The dynamic bin regions depend on the bin sizes, which are only known on
@@ -203,6 +203,9 @@ static Layout layout(long long n, long long m, long long nown, bool mg) {
     L.fbx = o; o = align_up(o + L.fbx_bytes, 256);
     // ELL4 rows (single GPU, every degree <= 4): 8 bytes per node
     L.ell = o; o = align_up(o + (mg ? 0 : 8 * (size_t)n), 256);
+    // live lower lists (single GPU): one int32 per half-edge + a count per node
+    L.lc = o; o = align_up(o + (mg ? 0 : 4 * (size_t)m), 256);
+    L.lcnt = o; o = align_up(o + (mg ? 0 : 4 * (size_t)n), 256);
     L.total = o;
     return L;
 }
@@ -220,8 +223,11 @@ static const void *pick(bool narrow, bool x16, bool c16) {
 // the instantiation for (offset width, state width, column format, bin-0
 // only, stats, ELL4 rows).  int64 offsets (m >= 2^31) keep 32-bit words.
 static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats, bool small = false,
-                                 bool plain = false, bool ell = false) {
+                                 bool plain = false, bool ell = false, bool live = false) {
     if (!narrow) x16 = c16 = false;
+    if (live && !small && !plain)
+        return stats ? pick<LF32, LF16, LF16D, LF32D, true>(narrow, x16, c16)
+                     : pick<LF32, LF16, LF16D, LF32D, false>(narrow, x16, c16);
     if (small && c16 && ell) {  // ELL4 rows imply int32 offsets and delta columns
         if (plain) return x16 ? kernel_ptr<int, PSEF16D, false>() : kernel_ptr<int, PSEF32D, false>();
         if (stats) return x16 ? kernel_ptr<int, SEF16D, true>() : kernel_ptr<int, SEF32D, true>();
@@ -261,7 +267,7 @@ static int occupancy() {
 // 16-bit state word, forbid 16-bit delta columns, the multi-GPU exchange mode.
 // Per host thread: a knob set by one caller never changes another thread's solves.
 static thread_local int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0, g_mg_exchange = 0,
-                        g_no_ell = 0;
+                        g_no_ell = 0, g_live = -1;
 
 // Per-solve preprocessing shared by hc_solve and hc_mg_solve, for the owned
 // range [lo, lo + nown): fresh control block, static degree-bucketed lists,
@@ -501,6 +507,12 @@ int hc_solve_set_l2_window(int allow) {
     return HC_OK;
 }
 
+int hc_solve_set_live(int mode) {
+    HC_REQUIRE(mode >= -1 && mode <= 1, HC_ERR_INVALID, "hc_solve_set_live: mode %d invalid", mode);
+    g_live = mode;
+    return HC_OK;
+}
+
 int hc_solve_set_ell(int allow) {
     g_no_ell = allow ? 0 : 1;
     return HC_OK;
@@ -576,6 +588,8 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
     P.X = reinterpret_cast<unsigned *>(ws + L.x);
     P.fb0 = reinterpret_cast<unsigned *>(ws + L.fb0);
     P.fbx = reinterpret_cast<unsigned *>(ws + L.fbx);
+    P.lc = reinterpret_cast<int *>(ws + L.lc);
+    P.lcnt = reinterpret_cast<int *>(ws + L.lcnt);
     P.rec = d_rec;
     P.max_rec = d_rec ? max_rec : 0;
     P.colors_out = reinterpret_cast<long long *>(d_colors);
@@ -599,6 +613,14 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
     // bin-0-only graphs (every degree <= 16) run the SMALL kernel
     bool small = !g_no_small;
     for (int k = 1; k < NKEY; ++k) small = small && pr.tot[k] == 0;
+    // live lower lists pay on skewed graphs large enough to be bandwidth-bound
+    // (RMAT-26 601 -> 435 ms, RMAT-22 31.4 -> 28.7 ms); ER-2^25 (no hubs) and
+    // RMAT-16 (latency-bound) measured slower with them
+    unsigned long long hubs = 0;
+    for (int k = 9; k < NKEY; ++k) hubs += pr.tot[k];
+    // (pure topology sweeps read the static rows and measured faster without)
+    const bool live =
+        g_live >= 0 ? g_live != 0 : (hubs > 0 && num_edges >= (1LL << 25) && mode != HC_MODE_TOPO);
     long long info[3];
     for (int attempt = 0;; ++attempt) {
         if (attempt > 0) {  // fresh control block (keeps nstat via copy_totals)
@@ -610,8 +632,9 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
                 HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
         }
         HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
+        HC_CUDA_TRY(cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)num_nodes, st));  // every live list: not scanned yet
         void *args[] = {&P};
-        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr, small, plain, pr.ell_ok);
+        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr, small, plain, pr.ell_ok, live);
         const int per_sm = occupancy_of(fn);
         HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
         P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
@@ -628,6 +651,7 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
         x16 = false;  // redo with 32-bit state words
     }
     if (h_rounds) *h_rounds = info[0];
+    HC_REQUIRE(info[1] != 2, HC_ERR_STALLED, "hc_solve: no convergence after %lld rounds (internal error)", info[0]);
     HC_REQUIRE(!info[1], HC_ERR_RECORDS, "hc_solve: %lld rounds exceed the %lld-record buffer",
                info[0], (long long)max_rec);
     return HC_OK;

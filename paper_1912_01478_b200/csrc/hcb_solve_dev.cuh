@@ -98,6 +98,12 @@ constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 #ifndef HC_PHASE_TIMES
 #define HC_PHASE_TIMES 0
 #endif
+#ifndef HC_LIVE
+#define HC_LIVE 1   // resolve scans of bins 1..4 compact each node's lower list to its uncolored entries
+#endif
+#ifndef HC_GROUP_PREFETCH
+#define HC_GROUP_PREFETCH 1   // resolve: group tiles fetch the next tile's entries one tile ahead
+#endif
 #ifndef HC_WARP_COMPACT
 #define HC_WARP_COMPACT 0   // bin-0 losers compacted per warp (order kept within a warp's run)
 #endif
@@ -191,6 +197,9 @@ constexpr int HA_WORDS = 62;                   // colors 65..2048 beyond the 64-
 #ifndef HC_MAX_SPLIT
 #define HC_MAX_SPLIT 1024
 #endif
+#ifndef HC_NO_SPLIT
+#define HC_NO_SPLIT 0   // experiments: never split hubs into slices
+#endif
 #ifndef HC_SPLIT_ANY
 #define HC_SPLIT_ANY 0   // split the active hubs whenever they fit the slots (not only when fewer than the CTAs)
 #endif
@@ -235,6 +244,17 @@ struct Params {
     // node's own bitmap instead of a scan of its adjacency.
     unsigned *fb0;
     unsigned *fbx;
+    // live lower lists (single GPU, bins 1..4): once u has been scanned in a
+    // data-driven round, its lower neighbours that were still uncolored then
+    // are lc[ro[u] .. ro[u] + live) (any order).  Resolve counts conflicts
+    // only against uncolored lower neighbours (a committed one never matches:
+    // T[u] avoids committed colors), and colored nodes never become
+    // uncolored, so a scan may drop every committed entry for good --
+    // compacted in place by the scan itself.  `live` travels in the list
+    // entry's od (bins 1..3: OD_LIVE | live << 48) or in lcnt[u] (hubs; -1:
+    // not scanned yet).
+    int *lc;
+    int *lcnt;
     long long lo, nown;        // owned node range [lo, lo + nown) (single GPU: 0, n)
     // multi-GPU (Fmt::mg) only
     const unsigned char *bnd;  // per owned node: bit q = rank q reads this word (global id index)
@@ -294,6 +314,7 @@ struct SmemT {
     int hub_first;
     unsigned unit;
     unsigned out_cnt;
+    unsigned kcnt;  // live-list compaction count (resolve_cta)
     unsigned mg_abort;
 };
 using Smem = SmemT<false>;
@@ -305,6 +326,14 @@ __device__ __forceinline__ int *dyn_list(const Params &P, int p, int b) {
 }
 __device__ __forceinline__ unsigned long long *dyn_od(const Params &P, int p, int b) {
     return p ? P.dyn_od[1][b] : P.dyn_od[0][b];
+}
+// od = row offset << 16 | degree (bits 16..47 and 0..15); bins 1..3 add the
+// live lower count (bits 48..62) under OD_LIVE once compacted
+constexpr unsigned long long OD_LIVE = 1ull << 63;
+constexpr unsigned long long OD_BASE = (1ull << 48) - 1ull;
+__device__ __forceinline__ long long od_off(unsigned long long od) { return (long long)((od >> 16) & 0xffffffffull); }
+__device__ __forceinline__ unsigned long long od_live(unsigned long long od, unsigned kept) {
+    return (od & OD_BASE) | OD_LIVE | ((unsigned long long)kept << 48);
 }
 __device__ __forceinline__ unsigned long long make_od(long long b, long long e) {
     return ((unsigned long long)b << 16) | (unsigned long long)(e - b);
@@ -497,7 +526,10 @@ __device__ bool mg_sync(const Params &P, SMT &sm, unsigned long long epoch, int 
 //               (grids): a node's whole adjacency is one 8-byte word (Params
 //               ell) loaded together with its state word -- no row offsets,
 //               no dependent column load
-template <typename XT, typename CT, bool MG = false, bool SMALL = false, bool PLAIN = false, bool ELL = false>
+//   LIVE        live lower lists (Params lc): resolve scans of bins 1..4 keep
+//               only the still-uncolored lower neighbours (skewed graphs)
+template <typename XT, typename CT, bool MG = false, bool SMALL = false, bool PLAIN = false, bool ELL = false,
+          bool LIVEL = false>
 struct Fmt {
     using xt = XT;
     using ct = CT;
@@ -505,7 +537,9 @@ struct Fmt {
     static constexpr bool small = SMALL;
     static constexpr bool plain = PLAIN;
     static constexpr bool ell = ELL;
+    static constexpr bool live = LIVEL;
     static_assert(!ELL || (SMALL && !MG && sizeof(CT) == 2), "ELL4 rows: bin-0-only, single GPU, delta columns");
+    static_assert(!LIVEL || (!SMALL && !MG && !PLAIN), "live lower lists: general single-GPU kernel");
 };
 using F32 = Fmt<unsigned, int>;
 using F16 = Fmt<unsigned short, int>;
@@ -535,6 +569,10 @@ using SEF16D = Fmt<unsigned short, short, false, true, false, true>;
 using SEF32D = Fmt<unsigned, short, false, true, false, true>;
 using PSEF16D = Fmt<unsigned short, short, false, true, true, true>;
 using PSEF32D = Fmt<unsigned, short, false, true, true, true>;
+using LF32 = Fmt<unsigned, int, false, false, false, false, true>;
+using LF16 = Fmt<unsigned short, int, false, false, false, false, true>;
+using LF16D = Fmt<unsigned short, short, false, false, false, false, true>;
+using LF32D = Fmt<unsigned, short, false, false, false, false, true>;
 
 // committed flag / color mask of the format's state word; words are kept
 // zero-extended in registers, so no conversion on load or store
@@ -664,6 +702,8 @@ __device__ __forceinline__ void mask_add(unsigned long long &mask, unsigned x) {
 #endif
 template <class F>
 constexpr bool FBM = HC_FBM && !F::mg;  // the multi-GPU solve keeps the adjacency-scan assign
+template <class F>
+constexpr bool LIVE = HC_LIVE && F::live;  // live lower lists (Params lc)
 
 #ifndef HC_FB_FILTER
 #define HC_FB_FILTER 1   // skip pushes into neighbours already committed (one X gather per push)
@@ -782,17 +822,40 @@ __device__ unsigned warp_mex_above64(const Params &P, int u, long long b, long l
     }
 }
 
-// One warp tile of a group bin: 32/G nodes, G lanes per node.
-template <int G, typename OffT, class F, bool STATS, int PHASE>
-__device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, const List &L,
-                                           const unsigned *prefix, unsigned long long v0,
-                                           unsigned long long hi, bool topo, int *out,
-                                           unsigned long long *out_od, unsigned *out_cnt, unsigned *bm,
-                                           unsigned &seg_hint,
-                                           unsigned long long &my_conf, unsigned long long *my_edges,
-                                           int np_plain = 0, int bin_plain = 0) {
-    const unsigned lane = lane_id();
-    const unsigned sub = lane % G, gi = lane / G;
+// Live-list compaction of one 4-slot batch of a group (LIVE resolve): the
+// lower entries whose word is still uncolored go to lc[b + kept ...] (any
+// order), group-wise prefix from ballots; `kept` is the group's running count.
+// `idx0`: this lane's slot-0 index in the scanned list; when the source is
+// lc itself an entry that does not move is not rewritten.
+template <int G, class F>
+__device__ __forceinline__ void live_keep(const Params &P, long long b, const int *nb, const unsigned *x, int u,
+                                          unsigned gmask, unsigned &kept, bool in_place, unsigned idx0) {
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const bool keep = nb[q] < u && !(x[q] & FB<F>);
+        const unsigned bal = __ballot_sync(FULL, keep) & gmask;
+        const unsigned at = kept + __popc(bal & lt);
+        if (keep && !(in_place && at == idx0 + q * G)) P.lc[b + at] = nb[q];
+        kept += __popc(bal);
+    }
+}
+
+// The list entry of a group tile's node: id, (offset, degree) and the
+// node's own state word (activity / tentative color).  Fetched one tile ahead
+// in resolve (group_sub) so the next tile's list round trip and own-word
+// round trip overlap this tile's column and neighbour-word gathers; X[u] is
+// written by u's own processing only, so the early read sees the same value.
+struct GEntry {
+    int u;
+    unsigned xu;
+    unsigned long long od;
+};
+template <int G, class F, int PHASE>
+__device__ __forceinline__ GEntry group_fetch(const Params &P, const List &L, const unsigned *prefix,
+                                              unsigned long long v0, unsigned long long hi, bool topo,
+                                              unsigned &seg_hint) {
+    const unsigned gi = lane_id() / G;
     const unsigned long long v = v0 + gi;
     // the list entry carries the adjacency range (no dependent row-offset load)
     // segment walk from the warp's hint (positions only grow along a chunk):
@@ -800,14 +863,31 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     unsigned sg = seg_hint;
     const long long idx = v < hi ? list_index_walk(L, prefix, v, sg) : -1;
     seg_hint = __shfl_sync(FULL, sg, 0);  // lane 0 holds the tile's first (smallest) position
-    int u = idx >= 0 ? ld_entry(L.base + idx) : -1;
-    const unsigned long long od = idx >= 0 ? ld_od(L.od + idx) : 0ull;
-    unsigned xu = 0;
-    if (topo || PHASE == 1) {
-        xu = u >= 0 ? xget<F>(P, u) : 0u;
-        if (topo && (xu & FB<F>)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
-    }
-    const long long b = u >= 0 ? (long long)(od >> 16) : 0;
+    GEntry g;
+    g.u = idx >= 0 ? ld_entry(L.base + idx) : -1;
+    g.od = idx >= 0 ? ld_od(L.od + idx) : 0ull;
+    g.xu = ((topo || PHASE == 1) && g.u >= 0) ? xget<F>(P, g.u) : 0u;
+    return g;
+}
+
+// One warp tile of a group bin: 32/G nodes, G lanes per node (`pre`: the
+// tile's entries, already fetched by group_fetch; nullptr: fetch here).
+template <int G, typename OffT, class F, bool STATS, int PHASE>
+__device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, const List &L,
+                                           const unsigned *prefix, unsigned long long v0,
+                                           unsigned long long hi, bool topo, int *out,
+                                           unsigned long long *out_od, unsigned *out_cnt, unsigned *bm,
+                                           unsigned &seg_hint,
+                                           unsigned long long &my_conf, unsigned long long *my_edges,
+                                           int np_plain = 0, int bin_plain = 0, const GEntry *pre = nullptr) {
+    const unsigned lane = lane_id();
+    const unsigned sub = lane % G, gi = lane / G;
+    const GEntry g = pre ? *pre : group_fetch<G, F, PHASE>(P, L, prefix, v0, hi, topo, seg_hint);
+    int u = g.u;
+    const unsigned long long od = g.od;
+    const unsigned xu = g.xu;
+    if (topo && (xu & FB<F>)) u = -1;  // inactive (_kernels.pyx:76-77, 135-136)
+    const long long b = u >= 0 ? od_off(od) : 0;
     const long long e = u >= 0 ? b + (long long)(od & 0xffffull) : 0;
     if constexpr (PHASE == 0 && FBM<F>) {
         // mex of the node's forbidden-color bitmap: word fb0[u] (one
@@ -834,10 +914,21 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
         }
         return;
     }
-    unsigned iters = (unsigned)((e - b + 4 * G - 1) / (4 * G));
+    // live lower list (data-driven resolve): scan lc[b, b + live) -- all
+    // below u, no exit test -- once u has been scanned (od carries the
+    // count), else the row with the early exit; the still-uncolored entries
+    // are compacted to lc[b, ...) and the loser's next od carries their count.
+    // (Topology sweeps read the static od: the row, no compaction.)
+    constexpr bool LV = LIVE<F> && PHASE == 1;
+    const bool lcomp = LV && !topo;
+    const bool lsrc = lcomp && (od & OD_LIVE);
+    const long long se = lsrc ? b + (long long)((od >> 48) & 0x7fffull) : e;  // end of the scanned range
+    unsigned iters = (unsigned)((se - b + 4 * G - 1) / (4 * G));
     iters = __reduce_max_sync(FULL, iters);
     unsigned long long mask = 0, mask2 = 0;  // colors 1..64, 65..128 (mask2: G == 32 only)
     unsigned cnt = 0, low = 0;
+    unsigned kept = 0;  // live entries written back (LV)
+    const unsigned gmask_lv = (G == 32) ? FULL : (((1u << (G & 31)) - 1u) << (gi * G));
     bool stop = u < 0;
     // software pipeline: the column ids of iteration it+1 are in flight while
     // the X gathers of iteration it are issued
@@ -846,7 +937,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const long long k = b + sub + q * G;
-        nb[q] = (!stop && k < e) ? colget<F>(P, k, u) : pad;
+        nb[q] = (!stop && k < se) ? (lsrc ? __ldcg(P.lc + k) : colget<F>(P, k, u)) : pad;
     }
     if constexpr (G < 32) {
         // bins 1 and 2: degree <= 4G, so the first column batch is the whole
@@ -861,6 +952,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
             for (int q = 0; q < 4; ++q)
                 if (nb[q] < u) { cnt += (x[q] & CM<F>) == xu; ++low; }
+            if (LV && lcomp) live_keep<G, F>(P, b, nb, x, u, gmask_lv, kept, lsrc, sub);
         }
         iters = 0;  // the loop below is skipped
     }
@@ -870,7 +962,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const long long k = kn + q * G;
-            nx[q] = (!stop && k < e) ? colget<F>(P, k, u) : pad;
+            nx[q] = (!stop && k < se) ? (lsrc ? __ldcg(P.lc + k) : colget<F>(P, k, u)) : pad;
         }
         if (PHASE == 0) {
             unsigned x[4];
@@ -895,6 +987,9 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
                 if (nb[q] < u) { cnt += (x[q] & CM<F>) == xu; ++low; }
                 else if (nb[q] != 0x7fffffff) ge = true;
             }
+            // in place: this batch's writes land below its own positions, the
+            // next batch is already in registers (nx)
+            if (LV && lcomp) live_keep<G, F>(P, b, nb, x, u, gmask_lv, kept, lsrc, it * 4u * G + sub);
             // adjacency sorted ascending (graph.py:193-197): once any lane of the
             // group saw a neighbour >= u, the group's later iterations are all >= u
             const unsigned bal = __ballot_sync(FULL, ge);
@@ -944,7 +1039,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
                 if constexpr (!F::plain) {
                     const unsigned pos = atomicAdd(out_cnt, 1u);  // the segment's global loser count
                     out[pos] = u;
-                    out_od[pos] = od;
+                    out_od[pos] = (LV && lcomp) ? od_live(od, kept) : od;
                     // multi-GPU: a global segment count (group_sub) bypasses seg_put's tally
                     if (F::mg && !__isShared(out_cnt)) atomicAdd(&s_wl_acc, 1ull);
                 }
@@ -955,10 +1050,22 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
         if constexpr (F::plain) plain_push<F>(P, np_plain, bin_plain, sub == 0 && u >= 0 && cnt != 0, u, od);
         if constexpr (FBM<F>) {
             if (u >= 0 && cnt == 0) {  // group-uniform: the winner's color goes into every neighbour's bitmap
-                if constexpr (G < 32) {  // the first column batch is the whole adjacency
+                if constexpr (G < 32) {
+                    if (lsrc) {  // nb held the live lower list: the whole row comes from the columns
+                        int w[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (nb[q] != 0x7fffffff) fb_push<F>(P, ro, nb[q], xu);
+                        for (int q = 0; q < 4; ++q) {
+                            const long long k = b + sub + q * G;
+                            w[q] = k < e ? colget<F>(P, k, u) : -1;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (w[q] >= 0) fb_push<F>(P, ro, w[q], xu);
+                    } else {  // the first column batch is the whole adjacency
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (nb[q] != 0x7fffffff) fb_push<F>(P, ro, nb[q], xu);
+                    }
                 } else {  // whole warp, one node: PU column loads per lane in flight
                     for (long long k0 = b + sub; k0 < e; k0 += (long long)PU * G) {
                         int w[PU];
@@ -1052,12 +1159,23 @@ __device__ unsigned assign_cta(const Params &P, const OffT *ro, int u, Smem &sm)
     }
 }
 
+// lcu: u's live lower count (>= 0: scan lc[b, b + lcu), all below u), or -1
+// (scan the row with the early exit).  compact: write the still-uncolored
+// entries back to lc[b, ...) in place -- one CTA barrier per chunk set so no
+// warp writes ahead of the entries another warp still has to read -- and
+// return their count in kept_out (LIVE).
 template <typename OffT, class F>
 __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned T, Smem &sm,
-                                unsigned &lower_out) {
+                                unsigned &lower_out, int lcu = -1, bool compact = false,
+                                unsigned *kept_out = nullptr) {
     const long long b = ro[u], e = ro[u + 1];
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-    if (threadIdx.x == 0) sm.red = 0;
+    const bool lsrc = LIVE<F> && lcu >= 0;  // CTA-uniform
+    const long long se = lsrc ? b + lcu : e;
+    if (threadIdx.x == 0) {
+        sm.red = 0;
+        sm.kcnt = 0;
+    }
     __syncthreads();
     unsigned cnt = 0, low = 0;
     // software pipeline: the next chunk's column ids are in flight while
@@ -1067,28 +1185,72 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
 #pragma unroll
     for (int q = 0; q < HU; ++q) {
         const long long k = b + (long long)warp * (32 * HU) + 32 * q + lane;
-        v[q] = k < e ? colget<F, true>(P, k, u) : 0x7fffffff;
+        v[q] = k < se ? (lsrc ? __ldcg(P.lc + k) : colget<F, true>(P, k, u)) : 0x7fffffff;
     }
-    for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
-        const bool more = __all_sync(FULL, v[HU - 1] < u);  // this chunk is wholly below u
-        int nv[HU];
+    if (LIVE<F> && (lsrc || compact)) {  // CTA-uniform
+        const long long nit = (se - b + 32LL * HU * NW - 1) / (32LL * HU * NW);
+        const unsigned lt = lanemask_lt();
+        // in place: every warp holds its first chunk before any warp writes
+        // (later chunk sets are loaded before the barrier that ends the
+        // previous iteration, and writes stay below the current set's end)
+        if (lsrc) __syncthreads();
+        for (long long it = 0; it < nit; ++it) {
+            const long long k0 = b + it * 32LL * HU * NW + (long long)warp * (32 * HU);
+            const bool more = lsrc || __all_sync(FULL, v[HU - 1] < u);  // this chunk is wholly below u
+            int nv[HU];
 #pragma unroll
-        for (int q = 0; q < HU; ++q) {
-            const long long k = k0 + 32LL * HU * NW + 32 * q + lane;
-            nv[q] = (more && k < e) ? colget<F, true>(P, k, u) : 0x7fffffff;
+            for (int q = 0; q < HU; ++q) {
+                const long long k = k0 + 32LL * HU * NW + 32 * q + lane;
+                nv[q] = (more && k < se) ? (lsrc ? __ldcg(P.lc + k) : colget<F, true>(P, k, u)) : 0x7fffffff;
+            }
+            unsigned x[HU];
+#pragma unroll
+            for (int q = 0; q < HU; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
+            bool stop = false;
+            unsigned bal[HU], wk = 0;
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
+                else stop = true;
+                bal[q] = __ballot_sync(FULL, compact && v[q] < u && !(x[q] & FB<F>));
+                wk += __popc(bal[q]);
+            }
+            unsigned base = 0;
+            if (lane == 0 && wk) base = atomicAdd(&sm.kcnt, wk);
+            base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                const unsigned at = base + __popc(bal[q] & lt);
+                const long long src = k0 - b + 32 * q + lane;  // this entry's index
+                if (((bal[q] >> lane) & 1u) && !(lsrc && (long long)at == src)) P.lc[b + at] = v[q];
+                base += __popc(bal[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < HU; ++q) v[q] = nv[q];
+            if (__syncthreads_or(stop)) break;  // later chunk sets are all >= u
         }
-        unsigned x[HU];
+    } else {
+        for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
+            const bool more = __all_sync(FULL, v[HU - 1] < u);  // this chunk is wholly below u
+            int nv[HU];
 #pragma unroll
-        for (int q = 0; q < HU; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
-        bool stop = false;
+            for (int q = 0; q < HU; ++q) {
+                const long long k = k0 + 32LL * HU * NW + 32 * q + lane;
+                nv[q] = (more && k < e) ? colget<F, true>(P, k, u) : 0x7fffffff;
+            }
+            unsigned x[HU];
 #pragma unroll
-        for (int q = 0; q < HU; ++q) {
-            if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
-            else stop = true;
+            for (int q = 0; q < HU; ++q) x[q] = v[q] < u ? xget<F>(P, v[q]) : 0u;
+            bool stop = false;
+#pragma unroll
+            for (int q = 0; q < HU; ++q) {
+                if (v[q] < u) { cnt += (x[q] & CM<F>) == T; ++low; }
+                else stop = true;
+            }
+#pragma unroll
+            for (int q = 0; q < HU; ++q) v[q] = nv[q];
+            if (__any_sync(FULL, stop)) break;  // later chunks are all >= u
         }
-#pragma unroll
-        for (int q = 0; q < HU; ++q) v[q] = nv[q];
-        if (__any_sync(FULL, stop)) break;  // later chunks are all >= u
     }
     cnt = warp_sum(cnt);
     low = warp_sum(low);
@@ -1096,6 +1258,7 @@ __device__ unsigned resolve_cta(const Params &P, const OffT *ro, int u, unsigned
     if (lane == 0 && (cnt | low)) atomicAdd(&sm.red, (unsigned long long)cnt | ((unsigned long long)low << 32));
     __syncthreads();
     const unsigned long long r = sm.red;
+    if (kept_out) *kept_out = sm.kcnt;
     __syncthreads();
     lower_out = (unsigned)(r >> 32);
     return (unsigned)r;
@@ -1182,7 +1345,7 @@ __device__ __forceinline__ void tile_issue(const Params &P, const OffT *ro, cons
             const long long idx = v < hi ? list_index_walk(L, prefix, v, seg) : -1;
             a.u[j] = idx >= 0 ? ld_entry(L.base + idx) : -1;
             const unsigned long long od = idx >= 0 ? ld_od(L.od + idx) : 0ull;
-            a.rb[j] = (OffT)(od >> 16);
+            a.rb[j] = (OffT)od_off(od);
             a.re[j] = a.rb[j] + (OffT)(od & 0xffffull);
         }
     }
@@ -1347,13 +1510,32 @@ __device__ __forceinline__ void group_sub(const Params &P, const OffT *ro, Smem 
         __syncthreads();
     }
     unsigned seg = lo < hi ? list_segment(rc.L[bin], sm.prefix[bin], lo) : 0u;  // once per unit
-    for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += (unsigned long long)NW * NG) {
-        const unsigned c = (unsigned)(v0 / csz);  // a warp tile never straddles segments (csz: whole tiles)
-        group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo,
-                                          dyn_list(P, np, bin) + (long long)c * csz,
-                                          dyn_od(P, np, bin) + (long long)c * csz,
-                                          whole ? &sm.out_cnt : &P.ctrl->segcnt[np][bin][c],
-                                          sm.win_bm[warp], seg, my_conf, my_edges, np, bin);
+    constexpr unsigned long long STEP = (unsigned long long)NW * NG;
+    if constexpr (PHASE == 1 && HC_GROUP_PREFETCH) {
+        // resolve: the next tile's entries are fetched before this tile runs
+        unsigned long long v0 = lo + (unsigned long long)warp * NG;
+        GEntry cur{-1, 0u, 0ull};
+        if (v0 < hi) cur = group_fetch<G, F, PHASE>(P, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo, seg);
+        for (; v0 < hi; v0 += STEP) {  // warp-uniform
+            GEntry nxt{-1, 0u, 0ull};
+            if (v0 + STEP < hi) nxt = group_fetch<G, F, PHASE>(P, rc.L[bin], sm.prefix[bin], v0 + STEP, hi, rc.topo, seg);
+            const unsigned c = (unsigned)(v0 / csz);  // a warp tile never straddles segments (csz: whole tiles)
+            group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo,
+                                              dyn_list(P, np, bin) + (long long)c * csz,
+                                              dyn_od(P, np, bin) + (long long)c * csz,
+                                              whole ? &sm.out_cnt : &P.ctrl->segcnt[np][bin][c],
+                                              sm.win_bm[warp], seg, my_conf, my_edges, np, bin, &cur);
+            cur = nxt;
+        }
+    } else {
+        for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += STEP) {
+            const unsigned c = (unsigned)(v0 / csz);  // a warp tile never straddles segments (csz: whole tiles)
+            group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo,
+                                              dyn_list(P, np, bin) + (long long)c * csz,
+                                              dyn_od(P, np, bin) + (long long)c * csz,
+                                              whole ? &sm.out_cnt : &P.ctrl->segcnt[np][bin][c],
+                                              sm.win_bm[warp], seg, my_conf, my_edges, np, bin);
+        }
     }
     if (whole) {
         __syncthreads();
@@ -1449,7 +1631,11 @@ __device__ unsigned assign_slice(const Params &P, const OffT *ro, int u, unsigne
 template <typename OffT, class F>
 __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsigned T, unsigned slice, unsigned k,
                                   HubAcc &acc, Smem &sm, bool &last, unsigned &low_out) {
-    const long long b0 = ro[u], e0 = ro[u + 1], len = e0 - b0;
+    // a hub already scanned once splits its live lower list lc[b0, b0 + lcnt)
+    // (all below u; read-only here: slices of other CTAs cannot compact in place)
+    const int lcu = LIVE<F> ? __ldcg(P.lcnt + u) : -1;
+    const bool lsrc = lcu >= 0;
+    const long long b0 = ro[u], e0 = lsrc ? b0 + lcu : ro[u + 1], len = e0 - b0;
     const long long b = b0 + len * slice / k, e = b0 + len * (slice + 1) / k;
     const unsigned warp = threadIdx.x >> 5, lane = lane_id();
     unsigned cnt = 0, low = 0;
@@ -1460,7 +1646,7 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
 #pragma unroll
     for (int q = 0; q < HU; ++q) {
         const long long kk = b + (long long)warp * (32 * HU) + 32 * q + lane;
-        v[q] = kk < e ? colget<F, true>(P, kk, u) : 0x7fffffff;
+        v[q] = kk < e ? (lsrc ? __ldcg(P.lc + kk) : colget<F, true>(P, kk, u)) : 0x7fffffff;
     }
     for (long long k0 = b + (long long)warp * (32 * HU); k0 < e; k0 += 32LL * HU * NW) {
         const bool more = __all_sync(FULL, v[HU - 1] < u);  // this chunk is wholly below u
@@ -1468,7 +1654,7 @@ __device__ unsigned resolve_slice(const Params &P, const OffT *ro, int u, unsign
 #pragma unroll
         for (int q = 0; q < HU; ++q) {
             const long long kk = k0 + 32LL * HU * NW + 32 * q + lane;
-            nv[q] = (more && kk < e) ? colget<F, true>(P, kk, u) : 0x7fffffff;
+            nv[q] = (more && kk < e) ? (lsrc ? __ldcg(P.lc + kk) : colget<F, true>(P, kk, u)) : 0x7fffffff;
         }
         unsigned x[HU];
 #pragma unroll
@@ -1700,9 +1886,25 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
         //      lists run in descending degree buckets), or every bin-3 node
         //      in the latency regime: one CTA per node
         const unsigned c = is_hub ? unit : unit - ub[1];
-        const int u = is_hub ? rc.L[BIN_HUB].base[c] : rc.L[3].base[list_index(rc.L[3], sm.prefix[3], c)];
+        const long long li = is_hub ? (long long)c : list_index(rc.L[3], sm.prefix[3], c);
+        const int u = is_hub ? rc.L[BIN_HUB].base[c] : rc.L[3].base[li];
         const unsigned xu = xget<F>(P, u);
         unsigned pushed = 0;
+        // live lower list: hubs keep the count in lcnt (any round); bin-3
+        // nodes in the list entry's od (data rounds; compaction there only)
+        int lcu = -1;
+        bool comp = false;
+        unsigned long long od3 = 0;
+        if (LIVE<F> && PHASE == 1) {
+            if (is_hub) {
+                lcu = __ldcg(P.lcnt + u);
+                comp = true;
+            } else if (!rc.topo) {
+                od3 = ld_od(rc.L[3].od + li);
+                lcu = (od3 & OD_LIVE) ? (int)((od3 >> 48) & 0x7fffull) : -1;
+                comp = true;
+            }
+        }
         if (!(rc.topo && (xu & FB<F>))) {  // topology sweep: inactive (_kernels.pyx:76)
             if (PHASE == 0) {
                 unsigned T;
@@ -1713,13 +1915,17 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                     if (STATS) my_edges[0] += ro[u + 1] - ro[u];
                 }
             } else {
-                unsigned low;
-                const unsigned k = resolve_cta<OffT, F>(P, ro, u, xu, sm, low);
+                unsigned low, kept = 0;
+                const unsigned k = resolve_cta<OffT, F>(P, ro, u, xu, sm, low, lcu, comp, &kept);
+                // a loser's next entry carries its live count (a winner's list is never read again)
+                const unsigned long long od_next = comp ? od_live(make_od(ro[u], ro[u + 1]), kept)
+                                                        : make_od(ro[u], ro[u + 1]);
                 if (threadIdx.x == 0) {
                     my_conf += k;
                     if (STATS) my_edges[1] += low;
                     if (k) {
                         if (is_hub) {
+                            if (comp) P.lcnt[u] = (int)kept;
                             dyn_list(P, np, BIN_HUB)[atomicAdd(&P.ctrl->hub_cnt[np], 1ull)] = u;
                         } else if constexpr (F::plain) {
                             const unsigned long long pos = atomicAdd(&P.ctrl->plain_cnt[np][3], 1ull);
@@ -1727,12 +1933,12 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                             dyn_od(P, np, 3)[pos] = make_od(ro[u], ro[u + 1]);
                         } else if (rc.bin3_by_cta) {  // segment c, capacity 1
                             dyn_list(P, np, 3)[c] = u;
-                            dyn_od(P, np, 3)[c] = make_od(ro[u], ro[u + 1]);
+                            dyn_od(P, np, 3)[c] = od_next;
                         } else {  // the segment of position c, through its global count
                             const unsigned sgm = c / rc.csz[3];
                             const long long at = (long long)sgm * rc.csz[3] + atomicAdd(&P.ctrl->segcnt[np][3][sgm], 1u);
                             dyn_list(P, np, 3)[at] = u;
-                            dyn_od(P, np, 3)[at] = make_od(ro[u], ro[u + 1]);
+                            dyn_od(P, np, 3)[at] = od_next;
                             if constexpr (F::mg) s_wl_acc += 1ull;
                         }
                         pushed = 1;
@@ -2019,7 +2225,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             // few active hubs (< nblocks): split them into edge slices; the
             // slice prefix is built below by the whole CTA
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;
-            rc.hub_split = (live && H > 0 && (HC_SPLIT_ANY || H < P.nblocks) && H <= MAX_SPLIT_SLOTS) ? 1u : 0u;
+            rc.hub_split = (!HC_NO_SPLIT && live && H > 0 && (HC_SPLIT_ANY || H < P.nblocks) && H <= MAX_SPLIT_SLOTS) ? 1u : 0u;
             rc.ubase[1] = live ? H : 0u;
             rc.ubase[2] = rc.ubase[1] + (live ? rc.k3 + rc.nsu[3] : 0u);
             rc.ubase[3] = rc.ubase[2] + (live ? rc.nsu[2] : 0u);
@@ -2036,6 +2242,13 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             // host redoes the solve with 32-bit words), never loop on a
             // truncated color
             sm.red = (!F::mg && __ldcg(P.fmt_overflow)) ? 0ull : sg;  // broadcast |W_t|
+            // every round commits at least the lowest-id active node, so a
+            // solve has at most n rounds; more means a broken invariant --
+            // stop (HC_ERR_STALLED) instead of looping forever
+            if (t > P.n + 1) {
+                sm.red = 0ull;
+                if (blockIdx.x == 0) C->rec_overflow = 2;
+            }
             if (blockIdx.x == 0) {
                 const unsigned long long now = globaltimer();
                 if (t > 1) {  // finish the record of round t-1 (driver.py:159-168)
@@ -2083,7 +2296,8 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             unsigned long long e_loc = 0;
             for (unsigned i = threadIdx.x; i < H; i += BLOCK) {
                 const int u = rc.L[BIN_HUB].base[i];
-                e_loc += (unsigned long long)(ro[u + 1] - ro[u]);
+                const int lcu = (LIVE<F> && FBM<F>) ? __ldcg(P.lcnt + u) : -1;  // resolve slices split the live list
+                e_loc += lcu >= 0 ? (unsigned long long)lcu : (unsigned long long)(ro[u + 1] - ro[u]);
             }
             e_loc = warp_sum(e_loc);
             if (threadIdx.x == 0) sm.red = 0;
@@ -2094,7 +2308,8 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             const unsigned long long S = max(4096ull, (sm.red + 2ull * P.nblocks - 1) / (2ull * P.nblocks));
             for (unsigned i = threadIdx.x; i < H; i += BLOCK) {
                 const int u = rc.L[BIN_HUB].base[i];
-                const unsigned long long d = (unsigned long long)(ro[u + 1] - ro[u]);
+                const int lcu = (LIVE<F> && FBM<F>) ? __ldcg(P.lcnt + u) : -1;
+                const unsigned long long d = lcu >= 0 ? (unsigned long long)lcu : (unsigned long long)(ro[u + 1] - ro[u]);
                 sm.hub_pre[i + 1] = (unsigned)max(1ull, (d + S - 1) / S);
             }
             if (threadIdx.x == 0) sm.hub_pre[0] = 0;
@@ -2168,7 +2383,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         C->rounds = t - 1;
-        if (t - 1 > P.max_rec) C->rec_overflow = 1;
+        if (t - 1 > P.max_rec && C->rec_overflow == 0) C->rec_overflow = 1;
         if constexpr (F::mg) P.mbox->last_epoch = ep;
     }
     for (long long i = gtid; i < P.nown; i += gthreads)
@@ -2197,9 +2412,11 @@ const void *kernel_ptr() {
 #define HC_INST_G8(X) \
     X(int, SEF16D, false) X(int, SEF32D, false) X(int, SEF16D, true) X(int, SEF32D, true) X(int, PSEF16D, false) \
     X(int, PSEF32D, false)
+#define HC_INST_G9(X) HC_SIX(X, L, false)
+#define HC_INST_G10(X) HC_SIX(X, L, true)
 #define HC_INST_ALL(X) \
     HC_INST_G0(X) HC_INST_G1(X) HC_INST_G2(X) HC_INST_G3(X) HC_INST_G4(X) HC_INST_G5(X) HC_INST_G6(X) HC_INST_G7(X) \
-    HC_INST_G8(X)
+    HC_INST_G8(X) HC_INST_G9(X) HC_INST_G10(X)
 
 }  // namespace solve
 }  // namespace hcb

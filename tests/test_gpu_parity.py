@@ -286,21 +286,23 @@ def test_forced_storage_formats_vs_golden(configs, fmt):
     L = hc._lib.load()
     L.hc_solve_set_formats(*fmt)
     try:
-        for small, ell in ((1, 1), (1, 0), (0, 1)):
+        for small, ell, live in ((1, 1, -1), (1, 0, -1), (0, 1, 0), (0, 1, 1)):
             L.hc_solve_set_small(small)
             L.hc_solve_set_ell(ell)
+            L.hc_solve_set_live(live)
             for key in ("rmat16", "grid64x96"):
                 kind, kw = CONFIG_SPECS[key]
                 want = configs[key]
                 dg = _device_graph(kind, kw)
                 for mode in MODES:
                     colors, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
-                    assert np.array_equal(colors, want["colors"]), (key, mode, fmt, small, ell)
-                    assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt, small, ell)
+                    assert np.array_equal(colors, want["colors"]), (key, mode, fmt, small, ell, live)
+                    assert np.array_equal(_recs(rep), want["rec"][mode]), (key, mode, fmt, small, ell, live)
     finally:
         L.hc_solve_set_formats(0, 0, 0)
         L.hc_solve_set_small(1)
         L.hc_solve_set_ell(1)
+        L.hc_solve_set_live(-1)
 
 
 # ---------------------------------------------------------------- unsorted caller CSR
