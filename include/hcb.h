@@ -169,6 +169,33 @@ int hc_solve_stats(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
                    hc_round_rec *d_rec, int64_t max_rec, int64_t *h_rounds, int64_t *d_stats,
                    void *d_ws, size_t ws_bytes, void *stream);
 
+/* Graph-capturable solve: a per-graph plan plus sync-free launches.
+ *
+ * hc_solve_plan runs the per-graph preprocessing of hc_solve once (degree
+ * binning, narrowed offsets, delta / ELL4 columns) into d_ws, reads the
+ * verdicts back (ONE host synchronisation) and fixes the kernel choice in
+ * *h_plan.  16-bit state words are planned only where they are exact
+ * (max degree <= 16384), so a launch never needs the 32-bit redo.
+ *
+ * hc_solve_launch then solves on the planned graph with stream-ordered work
+ * only (state reset, the cooperative solve kernel, the L2 demotion, a
+ * device-to-device copy of (rounds, record overflow / stall flag, format
+ * overflow) into d_info int64[3]): no host synchronisation, so it can be
+ * captured into a CUDA graph and replayed.  d_ws must be the planned
+ * workspace and the graph must be unchanged; results equal hc_solve's.
+ * d_info[1] != 0 means HC_ERR_RECORDS (1) or HC_ERR_STALLED (2). */
+typedef struct hc_solve_plan {
+    int64_t num_nodes, num_edges;
+    int32_t narrow, x16, c16, small, ell, live;
+    int64_t totals_offset;  /* bucket totals inside d_ws (copied into each launch's control block) */
+    int64_t reserved[3];
+} hc_solve_plan;
+int hc_solve_plan_graph(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                        int64_t num_edges, void *d_ws, size_t ws_bytes, hc_solve_plan *h_plan, void *stream);
+int hc_solve_launch(const hc_solve_plan *h_plan, const int64_t *d_row_offsets, const int32_t *d_col_indices,
+                    int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                    int64_t *d_info, void *d_ws, size_t ws_bytes, void *stream);
+
 /* Bench-only "Plain" data-driven baseline (the paper's IrGL Plain,
  * PAPER.md:268-283, 301-332): the same solve, but losers are pushed with
  * warp-aggregated atomics into one dense, unordered list per degree bin

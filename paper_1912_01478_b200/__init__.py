@@ -26,6 +26,7 @@ from .driver import (
     HybridConfig,
     RoundRecord,
     RunReport,
+    PlannedSolver,
     Solver,
     color_graph,
     colors_used,
@@ -74,7 +75,7 @@ __all__ = [
     "available_backends", "backend_name", "get_kernels",
     "ColorState", "RoundOutcome", "assign_color", "data_driven_iteration", "mex_positive",
     "resolve_conflicts", "topology_driven_iteration",
-    "MODES", "HybridConfig", "RoundRecord", "RunReport", "Solver",
+    "MODES", "HybridConfig", "RoundRecord", "RunReport", "Solver", "PlannedSolver",
     "color_graph", "colors_used", "threshold_count", "verify_coloring",
     "CsrGraph", "DeviceCsr", "EdgeList", "build_csr", "build_csr_device",
     "er_graph", "gen_er_edges", "gen_grid_edges", "gen_rmat_edges", "grid_graph",

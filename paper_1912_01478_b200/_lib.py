@@ -55,6 +55,15 @@ class RoundRec(ctypes.Structure):
 
 REC_FIELDS = 6  # int64 words per hc_round_rec
 
+
+class SolvePlan(ctypes.Structure):
+    """hc_solve_plan (include/hcb.h): the per-graph kernel choice of a planned workspace."""
+
+    _fields_ = [("num_nodes", ctypes.c_int64), ("num_edges", ctypes.c_int64),
+                ("narrow", ctypes.c_int32), ("x16", ctypes.c_int32), ("c16", ctypes.c_int32),
+                ("small", ctypes.c_int32), ("ell", ctypes.c_int32), ("live", ctypes.c_int32),
+                ("totals_offset", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)]
+
 _lib = None
 
 _i64 = ctypes.c_int64
@@ -81,6 +90,8 @@ _SIGS = {
     "hc_solve_set_live": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_plain": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
+    "hc_solve_plan_graph": (ctypes.c_int, [_p, _p, _i64, _i64, _p, ctypes.c_size_t, _p, _p]),
+    "hc_solve_launch": (ctypes.c_int, [_p, _p, _p, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_stats": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, _p, ctypes.c_size_t, _p]),
     "hc_mg_shared_bytes": (ctypes.c_size_t, [_i64]),
     "hc_mg_workspace_bytes": (ctypes.c_size_t, [_i64, _i64, _i64, _i64]),

@@ -284,16 +284,10 @@ struct Prep {
 };
 
 // ell: the ELL4 row array to fill (single GPU), nullptr on a multi-GPU rank
-static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_offsets, long long n,
-                   long long m, bool want_maxdeg, Prep &out, cudaStream_t st,
-                   unsigned long long *ell = nullptr) {
-    (void)n;
-    const bool narrow = m < 0x7fffffffLL && !g_force_wide;
-    out.narrow = narrow;
+// workspace pointers of a solve (prepare; hc_solve_launch re-binds a planned workspace)
+static void bind_params(Params &P, const Layout &L, char *ws, const int64_t *d_row_offsets, bool narrow) {
     P.ctrl = reinterpret_cast<Ctrl *>(ws + L.ctrl);
-    HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
     P.hub_acc = reinterpret_cast<HubAcc *>(ws + L.hub_acc);
-    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
     P.stat = reinterpret_cast<int *>(ws + L.stat);
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NBIN; ++b) P.dyn[p][b] = reinterpret_cast<int *>(ws + L.dyn[p][b]);
@@ -301,9 +295,22 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     for (int p = 0; p < 2; ++p)
         for (int b = 0; b < NSEG_BINS; ++b) P.dyn_od[p][b] = reinterpret_cast<unsigned long long *>(ws + L.dyn_od[p][b]);
     P.fmt_overflow = &P.ctrl->fmt_overflow;
+    const long long *ro_v = reinterpret_cast<const long long *>(d_row_offsets) - P.lo;  // indexed by global node id
+    P.ro = narrow ? (const void *)(reinterpret_cast<const int *>(ws + L.ro32) - P.lo) : (const void *)ro_v;
+    P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
+}
+
+static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_offsets, long long n,
+                   long long m, bool want_maxdeg, Prep &out, cudaStream_t st,
+                   unsigned long long *ell = nullptr) {
+    (void)n;
+    const bool narrow = m < 0x7fffffffLL && !g_force_wide;
+    out.narrow = narrow;
+    bind_params(P, L, ws, d_row_offsets, narrow);
+    HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
+    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
     const long long *ro_loc = reinterpret_cast<const long long *>(d_row_offsets);
     const long long *ro_v = ro_loc - P.lo;  // indexed by global node id (owned nodes only)
-    P.ro = narrow ? (const void *)(reinterpret_cast<const int *>(ws + L.ro32) - P.lo) : (const void *)ro_v;
     // static degree-bucketed lists of the owned nodes (bins contiguous, see DegreeKey)
     int rc = bucket_sort<NKEY>(P.nown, DegreeKey{ro_loc}, EmitI32{P.lo}, P.stat, ws + L.part,
                                &out.d_totals, st);
@@ -324,7 +331,6 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? align_up(2 * (size_t)m, 16) : 0));
     unsigned *ell_bad = bad + 1;
     HC_CUDA_TRY(cudaMemsetAsync(bad, 0, 2 * sizeof(unsigned), st));
-    P.ci16 = reinterpret_cast<const short *>(ws + L.ci16);
     P.ell = ell;
     if (narrow && m > 0 && P.nown > 0) {
         delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro_v, P.ci, P.lo, P.lo + P.nown,
@@ -561,6 +567,85 @@ int hc_solve_plain(const int64_t *d_row_offsets, const int32_t *d_col_indices, i
                       max_rec, h_rounds, nullptr, d_ws, ws_bytes, stream, true);
 }
 
+// per-solve fields of Params (single GPU)
+static void init_solve(Params &P, const Layout &L, char *ws, const int32_t *d_col_indices, long long n, int mode,
+                       long long thr_count, int64_t *d_colors, hc_round_rec *d_rec, long long max_rec,
+                       int64_t *d_stats) {
+    P.ci = d_col_indices;
+    P.n = n;
+    P.lo = 0;
+    P.nown = n;
+    P.X = reinterpret_cast<unsigned *>(ws + L.x);
+    P.fb0 = reinterpret_cast<unsigned *>(ws + L.fb0);
+    P.fbx = reinterpret_cast<unsigned *>(ws + L.fbx);
+    P.lc = reinterpret_cast<int *>(ws + L.lc);
+    P.lcnt = reinterpret_cast<int *>(ws + L.lcnt);
+    P.rec = d_rec;
+    P.max_rec = d_rec ? max_rec : 0;
+    P.colors_out = reinterpret_cast<long long *>(d_colors);
+    P.mode = mode;
+    P.thr = thr_count;
+    P.stats = reinterpret_cast<long long *>(d_stats);
+}
+
+// the kernel choice from the preprocessing verdicts (hc_solve: x16 may be
+// speculative; a plan keeps 16-bit words only where they are exact)
+struct Choice {
+    bool x16, x16_exact, c16, small, ell, live_ok;
+};
+static Choice choose(const Prep &pr, long long m) {
+    Choice c;
+    // 16-bit state words are exact when max degree <= 16384 (mex <= 16385;
+    // no node in the hub buckets >= 16385); above that they are used
+    // speculatively and the solve is redone with 32-bit words if any tentative
+    // color overflows (never for the BASELINE graphs)
+    c.x16_exact = pr.tot[9] + pr.tot[10] + pr.tot[11] + pr.tot[12] == 0;
+    c.x16 = (HC_FMT16 != 0) && !g_no_x16;
+    c.c16 = pr.c16_ok;
+    // bin-0-only graphs (every degree <= 16) run the SMALL kernel
+    c.small = !g_no_small;
+    for (int k = 1; k < NKEY; ++k) c.small = c.small && pr.tot[k] == 0;
+    c.ell = pr.ell_ok;
+    // live lower lists pay on skewed graphs large enough to be bandwidth-bound
+    // (RMAT-26 601 -> 435 ms, RMAT-22 31.4 -> 28.7 ms); ER-2^25 (no hubs) and
+    // RMAT-16 (latency-bound) measured slower with them
+    unsigned long long hubs = 0;
+    for (int k = 9; k < NKEY; ++k) hubs += pr.tot[k];
+    c.live_ok = g_live >= 0 ? g_live != 0 : (hubs > 0 && m >= (1LL << 25));
+    return c;
+}
+// (pure topology sweeps read the static rows and measured faster without live lists)
+static bool live_for(const Choice &c, int mode) { return c.live_ok && (g_live == 1 || mode != HC_MODE_TOPO); }
+
+// stream-ordered reset of the per-solve state and the cooperative launch
+// (no host synchronisation); info_dst: where the (rounds, record overflow /
+// stall, format overflow) triple is copied (host for hc_solve, device for
+// hc_solve_launch)
+static int launch_solve(Params &P, const Layout &L, const unsigned long long *d_totals, long long n, bool narrow,
+                        bool x16, bool c16, bool small, bool ell, bool live, bool plain, int64_t *d_stats,
+                        void *info_dst, cudaMemcpyKind info_kind, cudaStream_t st) {
+    HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
+    copy_totals_kernel<<<1, 32, 0, st>>>(d_totals, P.ctrl);
+    HC_CHECK_LAUNCH();
+    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
+    if (d_stats && P.max_rec)
+        HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
+    HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
+    HC_CUDA_TRY(cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)n, st));  // every live list: not scanned yet
+    void *args[] = {&P};
+    const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr, small, plain, ell, live);
+    const int per_sm = occupancy_of(fn);
+    HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
+    P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
+    bool windowed = false;
+    HC_CUDA_TRY(launch_persistent(fn, P.nblocks, args, st, P.X, (size_t)n * (x16 ? 2 : 4), true, &windowed));
+    // the persisting lines go back to normal: nothing of this solve stays
+    // pinned in L2 for the caller's next kernel (or the next solve)
+    if (windowed) HC_CUDA_TRY(l2_demote(P.X, (size_t)n * (x16 ? 2 : 4), st));
+    HC_CUDA_TRY(cudaMemcpyAsync(info_dst, &P.ctrl->rounds, 3 * sizeof(long long), info_kind, st));
+    return HC_OK;
+}
+
 static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
                       int64_t num_edges, int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec,
                       int64_t max_rec, int64_t *h_rounds, int64_t *d_stats, void *d_ws, size_t ws_bytes,
@@ -581,73 +666,21 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
                "hc_solve: workspace %zu bytes < required %zu", ws_bytes, L.total);
     char *ws = reinterpret_cast<char *>(d_ws);
     Params P{};
-    P.ci = d_col_indices;
-    P.n = num_nodes;
-    P.lo = 0;
-    P.nown = num_nodes;
-    P.X = reinterpret_cast<unsigned *>(ws + L.x);
-    P.fb0 = reinterpret_cast<unsigned *>(ws + L.fb0);
-    P.fbx = reinterpret_cast<unsigned *>(ws + L.fbx);
-    P.lc = reinterpret_cast<int *>(ws + L.lc);
-    P.lcnt = reinterpret_cast<int *>(ws + L.lcnt);
-    P.rec = d_rec;
-    P.max_rec = d_rec ? max_rec : 0;
-    P.colors_out = reinterpret_cast<long long *>(d_colors);
-    P.mode = mode;
-    P.thr = thr_count;
-    P.stats = reinterpret_cast<long long *>(d_stats);
-    if (d_stats && P.max_rec)
-        HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
+    init_solve(P, L, ws, d_col_indices, num_nodes, mode, thr_count, d_colors, d_rec, max_rec, d_stats);
     Prep pr;
     int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, false, pr, st,
                      reinterpret_cast<unsigned long long *>(ws + L.ell));
     if (rc != HC_OK) return rc;
-
-    // 16-bit state words are exact when max degree <= 16384 (mex <= 16385;
-    // no node in the hub buckets >= 16385); above that they are used
-    // speculatively and the solve is redone with 32-bit words if any tentative
-    // color overflows (never for the BASELINE graphs)
-    const bool x16_exact = pr.tot[9] + pr.tot[10] + pr.tot[11] + pr.tot[12] == 0;
-    bool x16 = (HC_FMT16 != 0) && !g_no_x16;
-    const bool c16 = pr.c16_ok;
-    // bin-0-only graphs (every degree <= 16) run the SMALL kernel
-    bool small = !g_no_small;
-    for (int k = 1; k < NKEY; ++k) small = small && pr.tot[k] == 0;
-    // live lower lists pay on skewed graphs large enough to be bandwidth-bound
-    // (RMAT-26 601 -> 435 ms, RMAT-22 31.4 -> 28.7 ms); ER-2^25 (no hubs) and
-    // RMAT-16 (latency-bound) measured slower with them
-    unsigned long long hubs = 0;
-    for (int k = 9; k < NKEY; ++k) hubs += pr.tot[k];
-    // (pure topology sweeps read the static rows and measured faster without)
-    const bool live =
-        g_live >= 0 ? g_live != 0 : (hubs > 0 && num_edges >= (1LL << 25) && mode != HC_MODE_TOPO);
+    const Choice ch = choose(pr, num_edges);
+    bool x16 = ch.x16;
     long long info[3];
-    for (int attempt = 0;; ++attempt) {
-        if (attempt > 0) {  // fresh control block (keeps nstat via copy_totals)
-            HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
-            copy_totals_kernel<<<1, 32, 0, st>>>(pr.d_totals, P.ctrl);
-            HC_CHECK_LAUNCH();
-            HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
-            if (d_stats && P.max_rec)
-                HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
-        }
-        HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
-        HC_CUDA_TRY(cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)num_nodes, st));  // every live list: not scanned yet
-        void *args[] = {&P};
-        const void *fn = select_kernel(pr.narrow, x16, c16, d_stats != nullptr, small, plain, pr.ell_ok, live);
-        const int per_sm = occupancy_of(fn);
-        HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
-        P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
-        bool windowed = false;
-        HC_CUDA_TRY(launch_persistent(fn, P.nblocks, args, st, P.X,
-                                      (size_t)num_nodes * (x16 ? 2 : 4), true, &windowed));
-        // the persisting lines go back to normal: nothing of this solve stays
-        // pinned in L2 for the caller's next kernel (or the next solve)
-        if (windowed) HC_CUDA_TRY(l2_demote(P.X, (size_t)num_nodes * (x16 ? 2 : 4), st));
-        HC_CUDA_TRY(cudaMemcpyAsync(info, &P.ctrl->rounds, sizeof info, cudaMemcpyDeviceToHost, st));
+    for (;;) {
+        rc = launch_solve(P, L, pr.d_totals, num_nodes, pr.narrow, x16, ch.c16, ch.small, ch.ell, live_for(ch, mode),
+                          plain, d_stats, info, cudaMemcpyDeviceToHost, st);
+        if (rc != HC_OK) return rc;
         HC_CUDA_TRY(cudaStreamSynchronize(st));
         const unsigned overflow = (unsigned)(info[2] & 0xffffffffLL);
-        if (!(x16 && overflow) || x16_exact) break;
+        if (!(x16 && overflow) || ch.x16_exact) break;
         x16 = false;  // redo with 32-bit state words
     }
     if (h_rounds) *h_rounds = info[0];
@@ -655,6 +688,67 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
     HC_REQUIRE(!info[1], HC_ERR_RECORDS, "hc_solve: %lld rounds exceed the %lld-record buffer",
                info[0], (long long)max_rec);
     return HC_OK;
+}
+
+int hc_solve_plan_graph(const int64_t *d_row_offsets, const int32_t *d_col_indices, int64_t num_nodes,
+                        int64_t num_edges, void *d_ws, size_t ws_bytes, hc_solve_plan *h_plan, void *stream) {
+    HC_REQUIRE(h_plan, HC_ERR_INVALID, "hc_solve_plan_graph: null plan");
+    HC_REQUIRE(num_nodes >= 0 && num_nodes < 0x7fffffffLL, HC_ERR_INVALID,
+               "hc_solve_plan_graph: num_nodes %lld out of range", (long long)num_nodes);
+    HC_REQUIRE(num_edges >= 0, HC_ERR_INVALID, "hc_solve_plan_graph: num_edges < 0");
+    memset(h_plan, 0, sizeof *h_plan);
+    h_plan->num_nodes = num_nodes;
+    h_plan->num_edges = num_edges;
+    if (num_nodes == 0) return HC_OK;
+    HC_REQUIRE(d_row_offsets && (num_edges == 0 || d_col_indices), HC_ERR_INVALID, "hc_solve_plan_graph: null pointer");
+    const Layout L = layout(num_nodes, num_edges, num_nodes, false);
+    HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
+               "hc_solve_plan_graph: workspace %zu bytes < required %zu", ws_bytes, L.total);
+    char *ws = reinterpret_cast<char *>(d_ws);
+    cudaStream_t st = as_stream(stream);
+    Params P{};
+    init_solve(P, L, ws, d_col_indices, num_nodes, HC_MODE_HYBRID, 0, nullptr, nullptr, 0, nullptr);
+    Prep pr;
+    const int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, false, pr, st,
+                           reinterpret_cast<unsigned long long *>(ws + L.ell));
+    if (rc != HC_OK) return rc;
+    const Choice ch = choose(pr, num_edges);
+    h_plan->narrow = pr.narrow;
+    h_plan->x16 = ch.x16 && ch.x16_exact;  // a launch never redoes the solve
+    h_plan->c16 = ch.c16;
+    h_plan->small = ch.small;
+    h_plan->ell = ch.ell;
+    h_plan->live = ch.live_ok;
+    h_plan->totals_offset = (int64_t)(reinterpret_cast<char *>(pr.d_totals) - ws);
+    return HC_OK;
+}
+
+int hc_solve_launch(const hc_solve_plan *h_plan, const int64_t *d_row_offsets, const int32_t *d_col_indices,
+                    int mode, int64_t thr_count, int64_t *d_colors, hc_round_rec *d_rec, int64_t max_rec,
+                    int64_t *d_info, void *d_ws, size_t ws_bytes, void *stream) {
+    HC_REQUIRE(h_plan && d_info, HC_ERR_INVALID, "hc_solve_launch: null plan / info");
+    HC_REQUIRE(mode >= HC_MODE_DATA && mode <= HC_MODE_HYBRID, HC_ERR_INVALID, "hc_solve_launch: mode %d invalid", mode);
+    HC_REQUIRE(max_rec >= 0, HC_ERR_INVALID, "hc_solve_launch: max_rec < 0");
+    cudaStream_t st = as_stream(stream);
+    const long long n = h_plan->num_nodes, m = h_plan->num_edges;
+    if (n == 0) {
+        HC_CUDA_TRY(cudaMemsetAsync(d_info, 0, 3 * sizeof(int64_t), st));
+        return HC_OK;
+    }
+    HC_REQUIRE(d_row_offsets && d_colors && (m == 0 || d_col_indices), HC_ERR_INVALID, "hc_solve_launch: null pointer");
+    const Layout L = layout(n, m, n, false);
+    HC_REQUIRE(d_ws && ws_bytes >= L.total, HC_ERR_WORKSPACE,
+               "hc_solve_launch: workspace %zu bytes < required %zu", ws_bytes, L.total);
+    char *ws = reinterpret_cast<char *>(d_ws);
+    Params P{};
+    init_solve(P, L, ws, d_col_indices, n, mode, thr_count, d_colors, d_rec, max_rec, nullptr);
+    bind_params(P, L, ws, d_row_offsets, h_plan->narrow != 0);
+    P.ell = reinterpret_cast<const unsigned long long *>(ws + L.ell);
+    Choice ch{};
+    ch.live_ok = h_plan->live != 0;
+    return launch_solve(P, L, reinterpret_cast<const unsigned long long *>(ws + h_plan->totals_offset), n,
+                        h_plan->narrow != 0, h_plan->x16 != 0, h_plan->c16 != 0, h_plan->small != 0,
+                        h_plan->ell != 0, live_for(ch, mode), false, nullptr, d_info, cudaMemcpyDeviceToDevice, st);
 }
 
 /* ---------------------------------------------------------------- multi-GPU */

@@ -2349,9 +2349,12 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             if (lane == 0 && v) atomicAdd(&sm.red, v);
             __syncthreads();
             if (threadIdx.x == 0 && sm.red) atomicAdd(&C->conflicts[p], sm.red);
-            if (F::mg && threadIdx.x == 0 && s_wl_acc) {
-                atomicAdd(&C->wl_next[np], s_wl_acc);
-                s_wl_acc = 0ull;
+            if (F::mg && threadIdx.x == 0) {  // (only thread 0 touches the tally here)
+                const unsigned long long w = s_wl_acc;
+                if (w) {
+                    atomicAdd(&C->wl_next[np], w);
+                    s_wl_acc = 0ull;
+                }
             }
             if (STATS) {
                 for (int q = 0; q < 2; ++q) {

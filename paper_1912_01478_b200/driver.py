@@ -182,6 +182,39 @@ class Solver:
         return DeviceSolve(self.colors[: g.num_nodes], recs, r, secs)
 
 
+class PlannedSolver(Solver):
+    """A solve that can be captured into a CUDA graph: the per-graph
+    preprocessing runs once (hc_solve_plan_graph, one host sync) and every
+    `launch` is stream-ordered work only (hc_solve_launch: state reset, the
+    persistent solve kernel, the (rounds, flags) triple copied into the device
+    tensor `info`).  `result` synchronises and reads the outcome."""
+
+    def __init__(self, graph: DeviceCsr, max_rec: int | None = None):
+        super().__init__(graph, max_rec)
+        g = self.g
+        self.plan = _lib.SolvePlan()
+        self.info = torch.zeros(3, dtype=torch.int64, device=graph.device)
+        _lib.check(self.L.hc_solve_plan_graph(
+            g.row_offsets.data_ptr(), _lib.ptr(g.col_indices), g.num_nodes, g.num_edges,
+            self.ws.data_ptr(), self.ws.numel(), ctypes.byref(self.plan), _lib.stream_handle()))
+
+    def launch(self, mode: str, thr_count: int, stream: torch.cuda.Stream | None = None) -> None:
+        g = self.g
+        _lib.check(self.L.hc_solve_launch(
+            ctypes.byref(self.plan), g.row_offsets.data_ptr(), _lib.ptr(g.col_indices), _lib.MODE_CODES[mode],
+            int(thr_count), self.colors.data_ptr(), self.rec.data_ptr(), self.max_rec, self.info.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(stream)))
+
+    def result(self) -> DeviceSolve:
+        torch.cuda.current_stream().synchronize()
+        rounds, flag, _ = (int(x) for x in self.info.cpu().tolist())
+        if flag == 2:
+            raise _lib.HcError(_lib.HC_ERR_STALLED, f"hc_solve_launch: no convergence after {rounds} rounds")
+        if flag:
+            raise _lib.HcError(_lib.HC_ERR_RECORDS, f"hc_solve_launch: {rounds} rounds exceed {self.max_rec} records")
+        return DeviceSolve(self.colors[: self.g.num_nodes], self.rec[:rounds].cpu().numpy(), rounds, float("nan"))
+
+
 def threshold_count(config: HybridConfig, num_nodes: int) -> int:
     """ceil(H * n) in host double arithmetic, exactly driver.py:138."""
     return math.ceil(config.threshold_fraction * num_nodes)

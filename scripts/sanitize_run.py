@@ -8,13 +8,18 @@ import paper_1912_01478_b200 as hc
 from oracle import oracle as O
 from paper_1912_01478_b200.pushbench import BenchConfig, run_push_bench
 
+from paper_1912_01478_b200 import _lib as _L0
+
 for scale in (8, 10):
     dg = hc.rmat_graph(scale, 16, 1)
     ro, ci = O.build_csr(1 << scale, O.gen_rmat(scale, 16, 1))
-    for mode in ("data", "topo", "hybrid"):
-        c, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
-        want, _ = O.color(ro, ci, mode)
-        assert np.array_equal(c, want)
+    for live in (-1, 1):  # per-graph default, then the live-lower-list instantiation forced
+        _L0.load().hc_solve_set_live(live)
+        for mode in ("data", "topo", "hybrid"):
+            c, rep = hc.color_graph(dg, hc.HybridConfig(mode=mode))
+            want, _ = O.color(ro, ci, mode)
+            assert np.array_equal(c, want)
+    _L0.load().hc_solve_set_live(-1)
 dg = hc.grid_graph(40, 30)
 c, rep = hc.color_graph(dg)
 # star hub (bin 4, split slices) + per-round plugin API + worklist sort

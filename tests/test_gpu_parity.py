@@ -372,3 +372,35 @@ def test_plain_baseline_same_results(corpus):
             b = s.run(mode, thr, plain=True)
             assert np.array_equal(ca, b.colors.cpu().numpy()), mode
             assert np.array_equal(a.records[:, 1:5], b.records[:, 1:5]), mode
+
+
+# ---------------------------------------------------------------- CUDA-graph capture
+@pytest.mark.parametrize("key", ["rmat16", "grid64x96"])
+def test_planned_launch_captured_in_cuda_graph(configs, key):
+    """hc_solve_plan_graph + hc_solve_launch: the launch is stream-ordered
+    work only, so it is captured into a CUDA graph; two replays (and an eager
+    launch) give the reference's colors and records (configs.npz goldens)."""
+    import torch
+
+    kind, kw = CONFIG_SPECS[key]
+    want = configs[key]
+    dg = _device_graph(kind, kw)
+    thr = hc.threshold_count(hc.HybridConfig(), dg.num_nodes)
+    ps = hc.PlannedSolver(dg)
+    ps.launch("hybrid", thr)  # eager
+    r = ps.result()
+    assert np.array_equal(r.colors.cpu().numpy(), want["colors"])
+    assert np.array_equal(r.records[:, 1:5], want["rec"]["hybrid"])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(graph, stream=s):
+            ps.launch("hybrid", thr, torch.cuda.current_stream())
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(2):
+        ps.colors.fill_(-1)
+        graph.replay()
+        r = ps.result()
+        assert np.array_equal(r.colors.cpu().numpy(), want["colors"]), key
+        assert np.array_equal(r.records[:, 1:5], want["rec"]["hybrid"]), key
