@@ -135,7 +135,10 @@ constexpr int HUB_MIN = 4097;            // deg >= HUB_MIN -> hub
 constexpr int HU = HC_HUB_U;             // column loads in flight per thread in the CTA-per-node paths
 constexpr int HUB_WORDS = 512;           // CTA bitmap window: 16384 colors per pass
 constexpr int WIN_WORDS = 32;            // warp bitmap window: 1024 colors per pass
-constexpr int MAXSEG = 2048;             // output segments per bin per round
+#ifndef HC_MAXSEG
+#define HC_MAXSEG 2048
+#endif
+constexpr int MAXSEG = HC_MAXSEG;        // output segments per bin per round
 static_assert(MAXSEG % BLOCK == 0, "prefix scan: whole items per thread");
 constexpr unsigned FBIT = 0x80000000u;
 constexpr unsigned CMASK = 0x7fffffffu;
@@ -2018,7 +2021,7 @@ __device__ __forceinline__ void run_phase(const Params &P, const OffT *ro, SMT &
                                           unsigned long long &my_conf, unsigned long long *my_edges) {
     // bitmap assign: its own unit space (no output lists; STATS builds keep
     // the binned path, which also counts the assign edges)
-    constexpr bool FA = PHASE == 0 && FBM<F> && !STATS;
+    constexpr bool FA = PHASE == 0 && FBM<F> && (!STATS || HC_PHASE_TIMES);  // (timing builds: the production assign)
     unsigned *ctr = &P.ctrl->unit_ctr[PHASE][p];
     if (threadIdx.x == 0) sm.unit = atomicAdd(ctr, 1u);
     __syncthreads();
