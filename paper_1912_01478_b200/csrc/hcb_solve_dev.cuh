@@ -2115,13 +2115,26 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
         // ---- current worklist sizes: rebuild the segment prefix of the
         //      previous round's output (round 1: the full static lists)
         if (!F::plain && t > 1) {
-#pragma unroll 1
-            for (int b = 0; b < NSB; ++b) {
-                const unsigned ns = rc.prev_nseg[b];
-                if (ns == 0) {  // CTA-uniform
-                    if (threadIdx.x == 0) sm.prefix[b][0] = 0;
-                    continue;
+            // bins with at most 32 segments (every bin in the latency regime):
+            // one warp each scans them with shuffles -- no CTA barriers
+            // (general kernel only: the bin-0-only kernel measured slower with it)
+            if (!F::small && warp < (unsigned)NSB) {
+                const unsigned ns = rc.prev_nseg[warp];
+                if (ns <= 32u) {
+                    const unsigned v = lane < ns ? __ldcg(&C->segcnt[p][warp][lane]) : 0u;
+                    const unsigned vi = warp_incl_scan(v);
+                    if (lane < ns) sm.prefix[warp][lane + 1] = vi;
+                    if (lane == 0) sm.prefix[warp][0] = 0;
                 }
+            }
+            bool big = F::small;
+#pragma unroll
+            for (int b = 0; b < NSB; ++b) big = big || rc.prev_nseg[b] > 32u;
+            if (!big) __syncthreads();
+#pragma unroll 1
+            for (int b = 0; big && b < NSB; ++b) {
+                const unsigned ns = rc.prev_nseg[b];
+                if (!F::small && ns <= 32u) continue;  // CTA-uniform: scanned by its warp above (before this loop's barriers)
                 for (unsigned s = threadIdx.x; s < ns; s += BLOCK)
                     sm.prefix[b][s + 1] = __ldcg(&C->segcnt[p][b][s]);
                 if (threadIdx.x == 0) sm.prefix[b][0] = 0;
