@@ -194,8 +194,11 @@ constexpr int HA_WORDS = 62;                   // colors 65..2048 beyond the 64-
 #ifndef HC_UPC3
 #define HC_UPC3 16   // bin-3 work units per CTA (at least one warp tile each)
 #endif
+#ifndef HC_BIN3_CTA
+#define HC_BIN3_CTA 0   // every bin-3 node CTA per node when at most 2 x #CTAs are active (RMAT-16 2.66 vs 2.32 ms without)
+#endif
 #ifndef HC_K3
-#define HC_K3 25   // leading bin-3 nodes taken CTA per node, in percent of the CTAs
+#define HC_K3 100  // leading bin-3 nodes taken CTA per node, in percent of the CTAs
 #endif
 #ifndef HC_MAX_SPLIT
 #define HC_MAX_SPLIT 1024
@@ -2191,7 +2194,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             const unsigned long long sg = !F::mg ? s : t == 1 ? (unsigned long long)P.n : __ldcg(&C->g_wl);
             const bool topo = P.mode == HC_MODE_TOPO || (P.mode == HC_MODE_HYBRID && (long long)sg > P.thr);
             // bin-3 nodes at CTA granularity when few are active (latency regime)
-            const bool bin3_cta = rc.L[3].total <= 2ull * P.nblocks;
+            const bool bin3_cta = HC_BIN3_CTA && rc.L[3].total <= 2ull * P.nblocks;
             if (topo)  // topology-driven: sweep the static lists, activity test
                 for (int b = 0; b < NBIN; ++b)
                     rc.L[b] = List{rc.stat_lists[b], rc.stat_od[b], rc.nst[b], 0, 0, false};
