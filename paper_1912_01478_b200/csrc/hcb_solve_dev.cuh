@@ -147,6 +147,13 @@ __host__ __device__ constexpr int bin_of_degree(long long d) {
     return d <= 16 ? 0 : d <= 32 ? 1 : d <= 64 ? 2 : d < HUB_MIN ? 3 : 4;
 }
 
+constexpr int MAX_PEND = 1024;
+#ifndef HC_DEFER_PUSH
+#define HC_DEFER_PUSH 1   // winning hubs' pushes split across every CTA at the next round start
+#endif
+#ifndef HC_DEFER_MIN
+#define HC_DEFER_MIN 65536   // ... for hubs of at least this degree
+#endif
 struct Ctrl {
     GridBarrier bar;
     int error;
@@ -155,7 +162,8 @@ struct Ctrl {
     unsigned long long hub_cnt[2];               // hub worklist size per parity
     unsigned long long conflicts[2];
     unsigned int unit_ctr[2][2];                 // [phase][parity]
-    long long rounds;
+    long long rounds_live;  // current round (development timing builds)
+    long long rounds;       // (rounds, rec_overflow, fmt_overflow) are read back as one triple
     long long rec_overflow;
     unsigned fmt_overflow;                       // a tentative color exceeded the state word
     unsigned pad1;
@@ -166,7 +174,12 @@ struct Ctrl {
     unsigned abort;
     unsigned pad2;
     unsigned long long plain_cnt[2][NSEG_BINS];  // Plain variant: dense list sizes per parity and bin
+    // winning hubs of a round whose bitmap pushes all CTAs share at the start
+    // of the next round (pend_cnt is reset after that; entries past MAX_PEND
+    // are pushed inline by their CTA)
+    unsigned pend_cnt[2];
     unsigned segcnt[2][NSEG_BINS][MAXSEG];       // [parity][bin][segment] loser counts
+    int pend[2][MAX_PEND];
 };
 
 // Multi-GPU mailbox, one per rank, in the rank's peer-mapped shared region
@@ -783,6 +796,18 @@ __device__ unsigned fb_mex_cta(const Params &P, const OffT *ro, int u, SMT &sm) 
 constexpr int PU = 8;
 template <typename OffT, class F>
 __device__ __forceinline__ void fb_push_row_cta(const Params &P, const OffT *ro, int u, unsigned c) {
+#if HC_PHASE_TIMES
+    const unsigned long long tp0 = globaltimer();
+    struct TP {  // development builds: longest CTA push of the round (stats column 6)
+        const Params &P;
+        unsigned long long t0;
+        __device__ ~TP() {
+            if (threadIdx.x == 0 && P.stats && P.ctrl->rounds_live >= 1 && P.ctrl->rounds_live <= P.max_rec)
+                atomicMax((unsigned long long *)&P.stats[5 * P.max_rec + 8 * (P.ctrl->rounds_live - 1) + 6],
+                          globaltimer() - t0);
+        }
+    } tp{P, tp0};
+#endif
     const long long b = ro[u], e = ro[u + 1];
     for (long long k0 = b + threadIdx.x; k0 < e; k0 += (long long)PU * BLOCK) {
         int v[PU];
@@ -797,6 +822,56 @@ __device__ __forceinline__ void fb_push_row_cta(const Params &P, const OffT *ro,
 #pragma unroll
         for (int q = 0; q < PU; ++q)
             if (!(x[q] & FB<F>)) fb_push<F, false>(P, ro, v[q], c);  // committed neighbours need none
+    }
+}
+
+// A winning hub's pushes: queued for the whole grid at the start of the next
+// round (one CTA walking a 10^4..10^6-entry row was the longest unit of the
+// RMAT tail rounds), or pushed here when the queue is full.  CTA-uniform.
+template <typename OffT, class F, class SMT>
+__device__ __forceinline__ void hub_push(const Params &P, const OffT *ro, SMT &sm, int p, int u, unsigned c) {
+    if constexpr (HC_DEFER_PUSH) {
+        if ((long long)(ro[u + 1] - ro[u]) < (long long)HC_DEFER_MIN) {  // CTA-uniform
+            fb_push_row_cta<OffT, F>(P, ro, u, c);
+            return;
+        }
+        if (threadIdx.x == 0) {
+            const unsigned i = atomicAdd(&P.ctrl->pend_cnt[p], 1u);
+            if (i < (unsigned)MAX_PEND) P.ctrl->pend[p][i] = u;
+            sm.hub_first = i < (unsigned)MAX_PEND ? 1 : 0;
+        }
+        __syncthreads();
+        const bool queued = sm.hub_first == 1;
+        __syncthreads();
+        if (queued) return;
+    }
+    fb_push_row_cta<OffT, F>(P, ro, u, c);
+}
+
+// The queued hub pushes of the previous round (parity q), every CTA a
+// contiguous share of the concatenated rows; the caller separates them from
+// the next assign with a grid barrier.  The hub's color is its committed word.
+template <typename OffT, class F, class SMT>
+__device__ void run_pending_pushes(const Params &P, const OffT *ro, SMT &sm, int q, unsigned npend) {
+    unsigned *pre = sm.hub_pre;  // scratch: the rows' prefix (hub split rebuilds it afterwards)
+    for (unsigned i = threadIdx.x; i < npend; i += BLOCK) {
+        const int h = __ldcg(&P.ctrl->pend[q][i]);
+        pre[i + 1] = (unsigned)(ro[h + 1] - ro[h]);
+    }
+    if (threadIdx.x == 0) pre[0] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (unsigned i = 1; i <= npend; ++i) pre[i] += pre[i - 1];
+    __syncthreads();
+    const unsigned long long total = pre[npend];
+    const unsigned long long share = (total + P.nblocks - 1) / P.nblocks;
+    const unsigned long long lo = min(total, (unsigned long long)blockIdx.x * share), hi = min(total, lo + share);
+    unsigned hub = 0;
+    for (unsigned long long g = lo + threadIdx.x; g < hi; g += BLOCK) {
+        while (pre[hub + 1] <= g) ++hub;  // positions grow along the loop
+        const int h = __ldcg(&P.ctrl->pend[q][hub]);
+        const unsigned c = xget<F>(P, h) & CM<F>;
+        fb_push<F>(P, ro, colget<F, true>(P, (long long)ro[h] + (long long)(g - pre[hub]), h), c);
     }
 }
 
@@ -1882,7 +1957,7 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                 else xput<F>(P, u, xu | FB<F>);
             }
             if constexpr (FBM<F>) {
-                if (last && kc == 0) fb_push_row_cta<OffT, F>(P, ro, u, xu);  // CTA-uniform
+                if (last && kc == 0) hub_push<OffT, F>(P, ro, sm, p, u, xu);  // CTA-uniform
             }
         }
         return;
@@ -1953,7 +2028,10 @@ __device__ __forceinline__ void run_unit(const Params &P, const OffT *ro, SMT &s
                     }
                 }
                 if constexpr (FBM<F>) {
-                    if (k == 0) fb_push_row_cta<OffT, F>(P, ro, u, xu);  // CTA-uniform
+                    if (k == 0) {  // CTA-uniform
+                        if (is_hub) hub_push<OffT, F>(P, ro, sm, p, u, xu);
+                        else fb_push_row_cta<OffT, F>(P, ro, u, xu);
+                    }
                 }
             }
         }
@@ -2291,6 +2369,7 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
                 }
                 t_start = now;
 #if HC_PHASE_TIMES
+                C->rounds_live = t;
                 if (STATS && t <= P.max_rec) P.stats[2 * P.max_rec + 3 * (t - 1)] = (long long)now;
 #endif
                 wl_in_prev = (long long)sg;
@@ -2309,6 +2388,16 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             // fills them is behind the next grid barrier)
             for (int b = 1; b < NSEG_BINS; ++b)
                 for (long long i = gtid; i < (long long)rc.nch[b]; i += gthreads) C->segcnt[np][b][i] = 0u;
+        }
+        if constexpr (FBM<F> && !F::small && HC_DEFER_PUSH) {
+            // the previous round's winning hubs: their pushes, shared by every
+            // CTA, then a barrier so this round's assign sees them
+            const unsigned npend = t > 1 ? min(__ldcg(&C->pend_cnt[np]), (unsigned)MAX_PEND) : 0u;
+            if (npend) {  // CTA-uniform
+                run_pending_pushes<OffT, F>(P, ro, sm, np, npend);
+                grid_sync(&C->bar, P.nblocks);
+                if (blockIdx.x == 0 && threadIdx.x == 0) C->pend_cnt[np] = 0;
+            }
         }
         if (!F::small && rc.hub_split) {  // CTA-uniform: equal-size edge slices over the active hubs
             const unsigned H = (unsigned)rc.L[BIN_HUB].total;

@@ -39,4 +39,4 @@ idx = list(range(min(6, R))) + list(range(6, R, max(1, R // 30)))
 for i in idx:
     print(f"  r{rec[i,0]:5d} {'topo' if rec[i,1] else 'data'} wl={rec[i,2]:9d} conf={rec[i,4]:10d} "
           f"Ea={ed[i,0]:11d} El={ed[i,1]:11d}  assign {a_us[i]:8.1f} us  resolve {r_us[i]:8.1f} us"
-          f"  | max unit hub {uk[i,0]:6.1f} b3 {uk[i,1]:6.1f} b2 {uk[i,2]:6.1f} b1 {uk[i,3]:6.1f} b0 {uk[i,4]:6.1f} busy {uk[i,5]:6.1f}")
+          f"  | max unit hub {uk[i,0]:6.1f} b3 {uk[i,1]:6.1f} b2 {uk[i,2]:6.1f} b1 {uk[i,3]:6.1f} b0 {uk[i,4]:6.1f} busy {uk[i,5]:6.1f} push {uk[i,6]:6.1f}")
