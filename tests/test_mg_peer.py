@@ -14,6 +14,7 @@ conflicts).
 
 import os
 import socket
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -289,3 +290,28 @@ def test_virtual_report_valid_and_colors_used():
     res = virtual_color_graph(dg, hc.HybridConfig(), 3)
     want, rep = hc.color_graph(dg)
     assert res.report.valid and res.report.colors_used == rep.colors_used
+
+
+def test_bench_two_ranks_share_gpu_line():
+    """bench.py's N>1 path end to end (torchrun, 2 ranks, per-rank CSR shards,
+    the peer-memory solve) with both ranks on cuda:0 (--share-gpu: gloo, the
+    persistent kernels time-slice): one JSON line from rank 0, a valid
+    coloring with RMAT-16's round count, half the CSR per rank."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--gpus", "2",
+           "--share-gpu", "--config", "rmat16", "--steps", "1", "--warmup", "3"]
+    out = subprocess.run(cmd, cwd=str(Path(__file__).resolve().parents[1]), env=env, capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-4000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["valid"] is True
+    assert line["config"]["rounds"] == 96
+    assert line["config"]["csr_shard_bytes_max"] < 0.7 * line["config"]["csr_bytes_total"]
