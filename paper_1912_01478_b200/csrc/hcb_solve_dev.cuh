@@ -104,9 +104,6 @@ constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 #ifndef HC_GROUP_PREFETCH
 #define HC_GROUP_PREFETCH 1   // resolve: group tiles fetch the next tile's entries one tile ahead
 #endif
-#ifndef HC_WARP_COMPACT
-#define HC_WARP_COMPACT 0   // bin-0 losers compacted per warp (order kept within a warp's run)
-#endif
 #ifndef HC_PAIR
 #define HC_PAIR 2   // bin-0-only kernel: tiles per loser-compaction barrier
 #endif
@@ -1809,10 +1806,6 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
     unsigned written = 0, buf = 0;
     // one segment search per chunk, then walks (not one search per tile)
     unsigned seg = (rc.ident || lo >= hi) ? 0u : list_segment(rc.L[0], sm.prefix[0], lo);
-    if (HC_WARP_COMPACT && !F::plain && PHASE == 1) {
-        if (threadIdx.x == 0) sm.out_cnt = 0;
-        __syncthreads();
-    }
     // the bin-0-only kernel compacts PAIR tiles per barrier
     constexpr int PAIR = F::small ? HC_PAIR : 1;
     constexpr int NS = PAIR * NP;  // slices per compaction
@@ -1847,28 +1840,6 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
                 if constexpr (!F::small) odj = odv[j];
                 plain_push<F>(P, np, 0, lost[j], u[j], odj);
             }
-        } else if (PHASE == 1 && HC_WARP_COMPACT) {
-            // warp-granular compaction: the warp's losers keep their order and
-            // take one shared-memory count per tile group (no CTA barrier;
-            // the warps' runs interleave in the segment in completion order)
-            unsigned bal[NS], tot = 0;
-#pragma unroll
-            for (int j = 0; j < NS; ++j) {
-                bal[j] = __ballot_sync(FULL, lost[j]);
-                tot += __popc(bal[j]);
-            }
-            unsigned run = 0;
-            if (lane == 0 && tot) run = atomicAdd(&sm.out_cnt, tot);
-            run = __shfl_sync(FULL, run, 0);
-#pragma unroll
-            for (int j = 0; j < NS; ++j) {
-                if (lost[j]) {
-                    const unsigned pos = run + __popc(bal[j] & lanemask_lt());
-                    out[pos] = u[j];
-                    if constexpr (!F::small) out_od[pos] = odv[j];
-                }
-                run += __popc(bal[j]);
-            }
         } else if (PHASE == 1) {
             unsigned bal[NS];
 #pragma unroll
@@ -1897,10 +1868,6 @@ __device__ __forceinline__ void bin0_chunk(const Params &P, const OffT *ro, SMT 
             written = run;
             buf ^= 1u;
         }
-    }
-    if (HC_WARP_COMPACT && !F::plain && PHASE == 1) {
-        __syncthreads();
-        written = sm.out_cnt;
     }
     if (!F::plain && PHASE == 1 && threadIdx.x == 0) seg_put<F::mg>(P, np, 0, c, written);
 }
