@@ -54,6 +54,14 @@ def _family(rng, kind):
             e.append(np.column_stack([np.full(d, h), rng.integers(0, n, d)]))
         e.append(rng.integers(0, n, (3 * n, 2)))
         return n, np.vstack(e)
+    if kind == "mega_hubs":  # hubs of degree >= 65536: their winning pushes are shared by every CTA
+        n = int(rng.integers(80000, 120000))
+        e = []
+        for h in rng.choice(n, int(rng.integers(1, 4)), replace=False):
+            d = int(rng.integers(66000, 90000))
+            e.append(np.column_stack([np.full(d, h), rng.integers(0, n, d)]))
+        e.append(rng.integers(0, n, (2 * n, 2)))
+        return n, np.vstack(e)
     if kind == "dense_core":  # a near-clique core: > 128 colors, seen by warp-per-node and hub nodes
         n = int(rng.integers(6000, 14000))
         core = rng.choice(n, int(rng.integers(500, 900)), replace=False)
@@ -70,7 +78,7 @@ def _family(rng, kind):
     raise ValueError(kind)
 
 
-KINDS = ("grid_shuffled", "cycles_paths", "mixed_degrees", "hubs", "dense_core", "rmat")
+KINDS = ("grid_shuffled", "cycles_paths", "mixed_degrees", "hubs", "mega_hubs", "dense_core", "rmat")
 
 
 @pytest.mark.parametrize("kind", KINDS)
