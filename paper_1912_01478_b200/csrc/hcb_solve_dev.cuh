@@ -98,6 +98,9 @@ constexpr int NPT = HC_NPT;              // bin-0 nodes per thread per tile
 #ifndef HC_PHASE_TIMES
 #define HC_PHASE_TIMES 0
 #endif
+#ifndef HC_LIVE_GROUPS
+#define HC_LIVE_GROUPS 0   // live lists also for bins 1-2 (8- and 16-lane groups): half the spills without (RMAT-26 422.5 -> 420.5 ms)
+#endif
 #ifndef HC_LIVE
 #define HC_LIVE 1   // resolve scans of bins 1..4 compact each node's lower list to its uncolored entries
 #endif
@@ -998,7 +1001,7 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
     // are compacted to lc[b, ...) and the loser's next od carries their count.
     // (Topology sweeps read the static od: the row, no compaction.)
     constexpr bool LV = LIVE<F> && PHASE == 1;
-    const bool lcomp = LV && !topo;
+    const bool lcomp = LV && !topo && (G == 32 || HC_LIVE_GROUPS);
     const bool lsrc = lcomp && (od & OD_LIVE);
     const long long se = lsrc ? b + (long long)((od >> 48) & 0x7fffull) : e;  // end of the scanned range
     unsigned iters = (unsigned)((se - b + 4 * G - 1) / (4 * G));
