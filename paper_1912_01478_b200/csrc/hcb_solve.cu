@@ -370,6 +370,9 @@ static std::unordered_map<void *, MgLaunch> g_mg_prepared;
 // Cooperative launch of the solve kernel with the state-word array as an L2
 // persisting access-policy window: the neighbour-word gathers are the reuse
 // the streamed column ids would otherwise evict (HC_L2_PERSIST=0 disables).
+#ifndef HC_L2_FRAC
+#define HC_L2_FRAC 3   // the window only when the array is below L2 / HC_L2_FRAC
+#endif
 #ifndef HC_L2_PERSIST
 #define HC_L2_PERSIST 1
 #endif
@@ -448,7 +451,7 @@ static cudaError_t launch_persistent(const void *fn, unsigned nblocks, void **ar
     // adds driver calls (RMAT-16: 2.9 -> 3.9 ms).  Grid4096 (33.5 MB of
     // words): 464 -> 443 ms with the window
     if (HC_L2_PERSIST && !g_no_l2_window && persist_max > 0 && xbytes >= ((size_t)16 << 20) &&
-        xbytes <= persist_max && 3 * xbytes < l2) {
+        xbytes <= persist_max && HC_L2_FRAC * xbytes < l2) {
         const size_t want = xbytes;
         cudaError_t e = cudaSuccess;
         if (limit_set_of[dev] != want) {  // exactly the array (a larger set-aside slowed the grid 590 -> 605 ms)

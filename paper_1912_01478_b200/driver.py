@@ -206,7 +206,8 @@ class PlannedSolver(Solver):
             self.ws.data_ptr(), self.ws.numel(), _lib.stream_handle(stream)))
 
     def result(self) -> DeviceSolve:
-        torch.cuda.current_stream().synchronize()
+        # the launch may have run on any stream (or as a replayed CUDA graph)
+        torch.cuda.synchronize(self.g.device)
         rounds, flag, _ = (int(x) for x in self.info.cpu().tolist())
         if flag == 2:
             raise _lib.HcError(_lib.HC_ERR_STALLED, f"hc_solve_launch: no convergence after {rounds} rounds")
