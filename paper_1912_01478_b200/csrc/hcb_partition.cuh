@@ -170,9 +170,17 @@ __global__ void __launch_bounds__(PART_THREADS) bucket_scatter_kernel(long long 
     const long long base = (long long)blockIdx.x * PART_TILE;
     for (int j = 0; j < PART_ITEMS; ++j) {
         const long long i = base + (long long)j * PART_THREADS + threadIdx.x;
-        if (i < count) {
-            const int b = key(i);
-            if (b >= 0) out[atomicAdd(&s_cur[b], 1ull)] = emit(i);
+        const int b = i < count ? key(i) : -1;
+        // warp-aggregated cursor bump: one shared atomic per (warp, bucket)
+        // instead of one per node (a tile of one bucket serialised 256
+        // same-address atomics per step)
+        const unsigned peers = __match_any_sync(FULL, b);
+        if (b >= 0) {
+            const int leader = __ffs(peers) - 1;
+            unsigned long long at = 0;
+            if ((int)lane_id() == leader) at = atomicAdd(&s_cur[b], (unsigned long long)__popc(peers));
+            at = __shfl_sync(peers, at, leader);
+            out[at + __popc(peers & lanemask_lt())] = emit(i);
         }
     }
 }

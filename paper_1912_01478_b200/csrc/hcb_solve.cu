@@ -55,8 +55,13 @@ __global__ void narrow_offsets_kernel(const long long *ro, int *ro32, long long 
 // first violation anywhere.  With ell != nullptr the same pass writes the ELL4 word
 // of every row of degree <= 4 (4 int16 deltas, row order, 0-padded) and sets
 // *ell_bad at the first row of degree > 4 (then the ELL4 kernel is not used).
+// Rows of more than 32 entries are only listed here (big_rows, *nbig) and
+// converted by delta_columns_big_kernel, one CTA per row: the hubs of an RMAT
+// graph have the lowest ids, so one warp walking its own 32 rows held the
+// whole pass (RMAT-16: nodes 0..31 hold 58.8 K entries, 139 us).
 __global__ void delta_columns_kernel(const long long *ro, const int *ci, long long lo, long long hi,
-                                     short *ci16, unsigned *bad, unsigned long long *ell, unsigned *ell_bad) {
+                                     short *ci16, unsigned *bad, unsigned long long *ell, unsigned *ell_bad,
+                                     int *big_rows, unsigned *nbig) {
     const unsigned lane = lane_id();
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long base = lo + (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); base < hi; base += stride) {
@@ -83,24 +88,38 @@ __global__ void delta_columns_kernel(const long long *ro, const int *ci, long lo
                 else if (!*(volatile unsigned *)ell_bad) atomicOr(ell_bad, 1u);
             }
         }
-        // rows longer than 32 entries: the whole warp, one row at a time
-        unsigned bigs = __ballot_sync(FULL, valid && big);
-        if (bigs && ell && !*(volatile unsigned *)ell_bad && lane == 0) atomicOr(ell_bad, 1u);
-        while (bigs && !__any_sync(FULL, fail)) {
-            const int src = __ffs(bigs) - 1;
-            bigs &= bigs - 1u;
-            const long long ur = base + src;
-            const long long br = __shfl_sync(FULL, b, src), er = __shfl_sync(FULL, e, src);
-            for (long long k = br + lane; k < er; k += 32) {
-                const long long d = (long long)ci[k] - ur;
-                if (d < -32768 || d > 32767) fail = true;
-                else ci16[k] = (short)d;
-            }
+        // rows longer than 32 entries: listed for delta_columns_big_kernel
+        const unsigned bigs = __ballot_sync(FULL, valid && big);
+        if (bigs) {
+            if (ell && !*(volatile unsigned *)ell_bad && lane == 0) atomicOr(ell_bad, 1u);
+            unsigned at = 0;
+            if (lane == 0) at = atomicAdd(nbig, (unsigned)__popc(bigs));
+            at = __shfl_sync(FULL, at, 0);
+            if (valid && big) big_rows[at + __popc(bigs & lanemask_lt())] = (int)u;
         }
         if (__any_sync(FULL, fail)) {
             if (lane == 0) atomicOr(bad, 1u);
             return;
         }
+    }
+}
+
+// the listed rows of more than 32 entries, one CTA per row (no barriers: a
+// CTA may stop part-way once some row failed)
+__global__ void delta_columns_big_kernel(const long long *ro, const int *ci, const int *big_rows,
+                                         const unsigned *nbig, short *ci16, unsigned *bad) {
+    const unsigned nr = *nbig;
+    for (unsigned r = blockIdx.x; r < nr; r += gridDim.x) {
+        if (*(volatile unsigned *)bad) return;
+        const long long u = big_rows[r];
+        const long long b = ro[u], e = ro[u + 1];
+        bool fail = false;
+        for (long long k = b + threadIdx.x; k < e; k += blockDim.x) {
+            const long long d = (long long)ci[k] - u;
+            if (d < -32768 || d > 32767) fail = true;
+            else ci16[k] = (short)d;
+        }
+        if (fail) atomicOr(bad, 1u);
     }
 }
 
@@ -330,11 +349,17 @@ static int prepare(Params &P, const Layout &L, char *ws, const int64_t *d_row_of
     // (behind the int16 columns, 16-byte aligned: a rank's shard can hold an odd number of half-edges)
     unsigned *bad = reinterpret_cast<unsigned *>(ws + L.ci16 + (narrow ? align_up(2 * (size_t)m, 16) : 0));
     unsigned *ell_bad = bad + 1;
-    HC_CUDA_TRY(cudaMemsetAsync(bad, 0, 2 * sizeof(unsigned), st));
+    unsigned *nbig = bad + 2;  // rows of > 32 entries, listed in the (not yet used) dynamic list of bin 0
+    HC_CUDA_TRY(cudaMemsetAsync(bad, 0, 3 * sizeof(unsigned), st));
     P.ell = ell;
     if (narrow && m > 0 && P.nown > 0) {
+        int *big_rows = reinterpret_cast<int *>(ws + L.dyn[1][0]);
         delta_columns_kernel<<<sms * 8, 256, 0, st>>>(ro_v, P.ci, P.lo, P.lo + P.nown,
-                                                      reinterpret_cast<short *>(ws + L.ci16), bad, ell, ell_bad);
+                                                      reinterpret_cast<short *>(ws + L.ci16), bad, ell, ell_bad,
+                                                      big_rows, nbig);
+        HC_CHECK_LAUNCH();
+        delta_columns_big_kernel<<<sms * 4, 256, 0, st>>>(ro_v, P.ci, big_rows, nbig,
+                                                          reinterpret_cast<short *>(ws + L.ci16), bad);
         HC_CHECK_LAUNCH();
     }
     unsigned long long *d_maxdeg = reinterpret_cast<unsigned long long *>(ws + L.maxdeg);
