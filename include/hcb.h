@@ -142,6 +142,10 @@ int hc_solve_set_small(int allow);
  * the CSR and run the ELL4 instantiation; allow = 0 forces the offset +
  * column path (per calling host thread; tests / experiments). */
 int hc_solve_set_ell(int allow);
+/* Graphs whose every degree is <= 128 (ER-2^25, grids) keep 8-bit state words
+ * (colors <= 127; a larger tentative color redoes the solve with 16-bit
+ * words); allow = 0 forces 16-bit words (per calling host thread). */
+int hc_solve_set_x8(int allow);
 /* Live lower lists (resolve keeps each node's still-uncolored lower
  * neighbours, compacted in place): mode -1 = per graph (hubs present and
  * >= 2^25 half-edges), 0 = off, 1 = on (per calling host thread). */

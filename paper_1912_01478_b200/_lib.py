@@ -87,6 +87,7 @@ _SIGS = {
     "hc_solve_set_small": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve_set_l2_window": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve_set_ell": (ctypes.c_int, [ctypes.c_int]),
+    "hc_solve_set_x8": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve_set_live": (ctypes.c_int, [ctypes.c_int]),
     "hc_solve": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),
     "hc_solve_plain": (ctypes.c_int, [_p, _p, _i64, _i64, ctypes.c_int, _i64, _p, _p, _i64, _p, _p, ctypes.c_size_t, _p]),

@@ -242,8 +242,15 @@ static const void *pick(bool narrow, bool x16, bool c16) {
 // the instantiation for (offset width, state width, column format, bin-0
 // only, stats, ELL4 rows).  int64 offsets (m >= 2^31) keep 32-bit words.
 static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats, bool small = false,
-                                 bool plain = false, bool ell = false, bool live = false) {
-    if (!narrow) x16 = c16 = false;
+                                 bool plain = false, bool ell = false, bool live = false, bool x8 = false) {
+    if (!narrow) x16 = c16 = x8 = false;
+    if (x8 && !stats && !live) {  // 8-bit state words (int32 offsets, no statistics build)
+        if (small && c16 && ell) return plain ? kernel_ptr<int, PSEF8D, false>() : kernel_ptr<int, SEF8D, false>();
+        if (small) return plain ? (c16 ? kernel_ptr<int, PSF8D, false>() : kernel_ptr<int, PSF8, false>())
+                                : (c16 ? kernel_ptr<int, SF8D, false>() : kernel_ptr<int, SF8, false>());
+        return plain ? (c16 ? kernel_ptr<int, PF8D, false>() : kernel_ptr<int, PF8, false>())
+                     : (c16 ? kernel_ptr<int, F8D, false>() : kernel_ptr<int, F8, false>());
+    }
     if (live && !small && !plain)
         return stats ? pick<LF32, LF16, LF16D, LF32D, true>(narrow, x16, c16)
                      : pick<LF32, LF16, LF16D, LF32D, false>(narrow, x16, c16);
@@ -285,6 +292,7 @@ static int occupancy() {
 // format overrides (tests / experiments): force int64 offsets, forbid the
 // 16-bit state word, forbid 16-bit delta columns, the multi-GPU exchange mode.
 // Per host thread: a knob set by one caller never changes another thread's solves.
+static thread_local int g_no_x8 = 0;
 static thread_local int g_force_wide = 0, g_no_x16 = 0, g_no_c16 = 0, g_no_small = 0, g_mg_exchange = 0,
                         g_no_ell = 0, g_live = -1;
 
@@ -530,6 +538,11 @@ int hc_solve_set_formats(int force_wide_offsets, int no_x16, int no_c16) {
     return HC_OK;
 }
 
+int hc_solve_set_x8(int allow) {
+    g_no_x8 = allow ? 0 : 1;
+    return HC_OK;
+}
+
 int hc_mg_set_exchange(int mode) {
     HC_REQUIRE(mode >= 0 && mode <= 2, HC_ERR_INVALID, "hc_mg_set_exchange: mode %d invalid", mode);
     g_mg_exchange = mode;
@@ -619,7 +632,7 @@ static void init_solve(Params &P, const Layout &L, char *ws, const int32_t *d_co
 // the kernel choice from the preprocessing verdicts (hc_solve: x16 may be
 // speculative; a plan keeps 16-bit words only where they are exact)
 struct Choice {
-    bool x16, x16_exact, c16, small, ell, live_ok;
+    bool x8, x16, x16_exact, c16, small, ell, live_ok;
 };
 static Choice choose(const Prep &pr, long long m) {
     Choice c;
@@ -629,6 +642,13 @@ static Choice choose(const Prep &pr, long long m) {
     // color overflows (never for the BASELINE graphs)
     c.x16_exact = pr.tot[9] + pr.tot[10] + pr.tot[11] + pr.tot[12] == 0;
     c.x16 = (HC_FMT16 != 0) && !g_no_x16;
+    // 8-bit state words (colors <= 127) when every degree is <= 128: exact up
+    // to degree 126 (mex <= deg + 1); a tentative color above 127 (two
+    // degrees only) flags the overflow and the solve is redone with 16 bits.
+    // ER-2^25: the 33.5 MB state array stays L2-resident (16-bit: 67 MB)
+    bool upto128 = true;
+    for (int k = 3; k < NKEY; ++k) upto128 = upto128 && (k == 8 || pr.tot[k] == 0);
+    c.x8 = c.x16 && !g_no_x8 && upto128;
     c.c16 = pr.c16_ok;
     // bin-0-only graphs (every degree <= 16) run the SMALL kernel
     c.small = !g_no_small;
@@ -651,7 +671,7 @@ static bool live_for(const Choice &c, int mode) { return c.live_ok && (g_live ==
 // hc_solve_launch)
 static int launch_solve(Params &P, const Layout &L, const unsigned long long *d_totals, long long n, bool narrow,
                         bool x16, bool c16, bool small, bool ell, bool live, bool plain, int64_t *d_stats,
-                        void *info_dst, cudaMemcpyKind info_kind, cudaStream_t st) {
+                        void *info_dst, cudaMemcpyKind info_kind, cudaStream_t st, bool x8 = false) {
     HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
     copy_totals_kernel<<<1, 32, 0, st>>>(d_totals, P.ctrl);
     HC_CHECK_LAUNCH();
@@ -661,15 +681,17 @@ static int launch_solve(Params &P, const Layout &L, const unsigned long long *d_
     HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
     HC_CUDA_TRY(cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)n, st));  // every live list: not scanned yet
     void *args[] = {&P};
-    const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr, small, plain, ell, live);
+    x8 = x8 && narrow && d_stats == nullptr && !live;  // (the instantiations select_kernel has)
+    const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr, small, plain, ell, live, x8);
+    const size_t xbytes = (size_t)n * (x8 ? 1 : x16 && narrow ? 2 : 4);
     const int per_sm = occupancy_of(fn);
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
     bool windowed = false;
-    HC_CUDA_TRY(launch_persistent(fn, P.nblocks, args, st, P.X, (size_t)n * (x16 ? 2 : 4), true, &windowed));
+    HC_CUDA_TRY(launch_persistent(fn, P.nblocks, args, st, P.X, xbytes, true, &windowed));
     // the persisting lines go back to normal: nothing of this solve stays
     // pinned in L2 for the caller's next kernel (or the next solve)
-    if (windowed) HC_CUDA_TRY(l2_demote(P.X, (size_t)n * (x16 ? 2 : 4), st));
+    if (windowed) HC_CUDA_TRY(l2_demote(P.X, xbytes, st));
     HC_CUDA_TRY(cudaMemcpyAsync(info_dst, &P.ctrl->rounds, 3 * sizeof(long long), info_kind, st));
     return HC_OK;
 }
@@ -700,14 +722,18 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
                      reinterpret_cast<unsigned long long *>(ws + L.ell));
     if (rc != HC_OK) return rc;
     const Choice ch = choose(pr, num_edges);
-    bool x16 = ch.x16;
+    bool x16 = ch.x16, x8 = ch.x8;
     long long info[3];
     for (;;) {
         rc = launch_solve(P, L, pr.d_totals, num_nodes, pr.narrow, x16, ch.c16, ch.small, ch.ell, live_for(ch, mode),
-                          plain, d_stats, info, cudaMemcpyDeviceToHost, st);
+                          plain, d_stats, info, cudaMemcpyDeviceToHost, st, x8);
         if (rc != HC_OK) return rc;
         HC_CUDA_TRY(cudaStreamSynchronize(st));
         const unsigned overflow = (unsigned)(info[2] & 0xffffffffLL);
+        if (x8 && overflow && pr.narrow && !d_stats && !live_for(ch, mode)) {
+            x8 = false;  // redo with 16-bit state words
+            continue;
+        }
         if (!(x16 && overflow) || ch.x16_exact) break;
         x16 = false;  // redo with 32-bit state words
     }

@@ -592,11 +592,23 @@ using LF32 = Fmt<unsigned, int, false, false, false, false, true>;
 using LF16 = Fmt<unsigned short, int, false, false, false, false, true>;
 using LF16D = Fmt<unsigned short, short, false, false, false, false, true>;
 using LF32D = Fmt<unsigned, short, false, false, false, false, true>;
+// 8-bit state words (colors <= 127): graphs of max degree <= 128 (ER-2^25,
+// grids); the whole state array stays L2-resident at twice the node count
+using F8 = Fmt<unsigned char, int>;
+using F8D = Fmt<unsigned char, short>;
+using SF8 = Fmt<unsigned char, int, false, true>;
+using SF8D = Fmt<unsigned char, short, false, true>;
+using SEF8D = Fmt<unsigned char, short, false, true, false, true>;
+using PF8 = Fmt<unsigned char, int, false, false, true>;
+using PF8D = Fmt<unsigned char, short, false, false, true>;
+using PSF8 = Fmt<unsigned char, int, false, true, true>;
+using PSF8D = Fmt<unsigned char, short, false, true, true>;
+using PSEF8D = Fmt<unsigned char, short, false, true, true, true>;
 
 // committed flag / color mask of the format's state word; words are kept
 // zero-extended in registers, so no conversion on load or store
 template <class F>
-constexpr unsigned FB = sizeof(typename F::xt) == 4 ? 0x80000000u : 0x8000u;
+constexpr unsigned FB = sizeof(typename F::xt) == 4 ? 0x80000000u : sizeof(typename F::xt) == 2 ? 0x8000u : 0x80u;
 template <class F>
 constexpr unsigned CM = FB<F> - 1u;
 
@@ -671,7 +683,7 @@ __device__ void zone_copy(const Params &P) {
 // for degree > 32766); flag it, the host reruns the solve with 32-bit words
 template <class F>
 __device__ __forceinline__ void xput_t(const Params &P, long long v, unsigned T) {
-    if (sizeof(typename F::xt) == 2 && T > CM<F>) *P.fmt_overflow = 1u;
+    if (sizeof(typename F::xt) < 4 && T > CM<F>) *P.fmt_overflow = 1u;
     xput<F>(P, v, T);
 }
 // load of a column id.  Low-degree rows are streamed (evict-first, so the
@@ -2495,9 +2507,11 @@ const void *kernel_ptr() {
     X(int, PSEF32D, false)
 #define HC_INST_G9(X) HC_SIX(X, L, false)
 #define HC_INST_G10(X) HC_SIX(X, L, true)
+#define HC_INST_G11(X) X(int, F8, false) X(int, F8D, false) X(int, SF8, false) X(int, SF8D, false) X(int, SEF8D, false)
+#define HC_INST_G12(X) X(int, PF8, false) X(int, PF8D, false) X(int, PSF8, false) X(int, PSF8D, false) X(int, PSEF8D, false)
 #define HC_INST_ALL(X) \
     HC_INST_G0(X) HC_INST_G1(X) HC_INST_G2(X) HC_INST_G3(X) HC_INST_G4(X) HC_INST_G5(X) HC_INST_G6(X) HC_INST_G7(X) \
-    HC_INST_G8(X) HC_INST_G9(X) HC_INST_G10(X)
+    HC_INST_G8(X) HC_INST_G9(X) HC_INST_G10(X) HC_INST_G11(X) HC_INST_G12(X)
 
 }  // namespace solve
 }  // namespace hcb

@@ -10,7 +10,7 @@ torch.cuda.set_device(0)
 L = hc._lib.load()
 for kv in sys.argv[2].split(":") if len(sys.argv) > 2 and sys.argv[2] else []:
     k, v = kv.split("=")
-    {"ell": L.hc_solve_set_ell, "small": L.hc_solve_set_small, "l2": L.hc_solve_set_l2_window, "live": L.hc_solve_set_live}[k](int(v))
+    {"ell": L.hc_solve_set_ell, "small": L.hc_solve_set_small, "l2": L.hc_solve_set_l2_window, "live": L.hc_solve_set_live, "x8": L.hc_solve_set_x8}[k](int(v))
 for w in sys.argv[1].split(","):
     dg = hc.grid_graph(int(w[4:]), int(w[4:])) if w.startswith("grid") else (hc.rmat_graph(int(w[4:])) if w.startswith("rmat") else hc.er_graph(1 << int(w[2:]), 32))
     s = hc.Solver(dg); thr = hc.threshold_count(hc.HybridConfig(), dg.num_nodes)

@@ -305,6 +305,31 @@ def test_forced_storage_formats_vs_golden(configs, fmt):
         L.hc_solve_set_live(-1)
 
 
+@pytest.mark.parametrize("x8", [1, 0])
+def test_8bit_state_words_vs_oracle(x8):
+    """8-bit state words (every degree <= 128) against the oracle, and with
+    them forbidden: ER graphs of max degree ~60-110, a grid (the ELL4 and
+    bin-0-only kernels), and cliques K_128 / K_129 whose last tentative colors
+    (128, 129) overflow 8 bits, so the solve is redone with 16-bit words."""
+    L = hc._lib.load()
+    L.hc_solve_set_x8(x8)
+    try:
+        cases = [(4000, O.gen_er(4000, 4000 * 30, 5)), (3000, O.gen_er(3000, 3000 * 40, 6)),
+                 (64 * 96, O.gen_grid(64, 96))]
+        for k in (128, 129):
+            iu, ju = np.triu_indices(k, 1)
+            cases.append((k, np.stack([iu, ju], 1).astype(np.int64)))
+        for n, e in cases:
+            ro, ci = O.build_csr(n, e)
+            g = hc.CsrGraph(n, len(ci), ro, ci).to_device()
+            for mode in MODES:
+                want, rec = O.color(ro, ci, mode)
+                colors, rep = hc.color_graph(g, hc.HybridConfig(mode=mode))
+                assert np.array_equal(colors, want) and np.array_equal(_recs(rep), rec), (n, mode, x8)
+    finally:
+        L.hc_solve_set_x8(1)
+
+
 # ---------------------------------------------------------------- unsorted caller CSR
 def _shuffle_rows(ro, ci, rng):
     ci = ci.copy()
