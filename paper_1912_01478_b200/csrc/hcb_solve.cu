@@ -244,10 +244,7 @@ static const void *pick(bool narrow, bool x16, bool c16) {
 static const void *select_kernel(bool narrow, bool x16, bool c16, bool stats, bool small = false,
                                  bool plain = false, bool ell = false, bool live = false, bool x8 = false) {
     if (!narrow) x16 = c16 = x8 = false;
-    if (x8 && !stats && !live) {  // 8-bit state words (int32 offsets, no statistics build)
-        if (small && c16 && ell) return plain ? kernel_ptr<int, PSEF8D, false>() : kernel_ptr<int, SEF8D, false>();
-        if (small) return plain ? (c16 ? kernel_ptr<int, PSF8D, false>() : kernel_ptr<int, PSF8, false>())
-                                : (c16 ? kernel_ptr<int, SF8D, false>() : kernel_ptr<int, SF8, false>());
+    if (x8 && !stats && !live && !small) {  // 8-bit state words (general kernel, int32 offsets, no statistics)
         return plain ? (c16 ? kernel_ptr<int, PF8D, false>() : kernel_ptr<int, PF8, false>())
                      : (c16 ? kernel_ptr<int, F8D, false>() : kernel_ptr<int, F8, false>());
     }
@@ -642,17 +639,18 @@ static Choice choose(const Prep &pr, long long m) {
     // color overflows (never for the BASELINE graphs)
     c.x16_exact = pr.tot[9] + pr.tot[10] + pr.tot[11] + pr.tot[12] == 0;
     c.x16 = (HC_FMT16 != 0) && !g_no_x16;
-    // 8-bit state words (colors <= 127) when every degree is <= 128: exact up
+    c.c16 = pr.c16_ok;
+    // bin-0-only graphs (every degree <= 16) run the SMALL kernel
+    c.small = !g_no_small;
+    for (int k = 1; k < NKEY; ++k) c.small = c.small && pr.tot[k] == 0;
+    // 8-bit state words (colors <= 127) when every degree is <= 128 (general
+    // kernel only: bin-0-only graphs measured faster with 16 bits): exact up
     // to degree 126 (mex <= deg + 1); a tentative color above 127 (two
     // degrees only) flags the overflow and the solve is redone with 16 bits.
     // ER-2^25: the 33.5 MB state array stays L2-resident (16-bit: 67 MB)
     bool upto128 = true;
     for (int k = 3; k < NKEY; ++k) upto128 = upto128 && (k == 8 || pr.tot[k] == 0);
-    c.x8 = c.x16 && !g_no_x8 && upto128;
-    c.c16 = pr.c16_ok;
-    // bin-0-only graphs (every degree <= 16) run the SMALL kernel
-    c.small = !g_no_small;
-    for (int k = 1; k < NKEY; ++k) c.small = c.small && pr.tot[k] == 0;
+    c.x8 = c.x16 && !g_no_x8 && upto128 && !c.small;
     c.ell = pr.ell_ok;
     // live lower lists pay on skewed graphs large enough to be bandwidth-bound
     // (RMAT-26 601 -> 435 ms, RMAT-22 31.4 -> 28.7 ms); ER-2^25 (no hubs) and
@@ -681,7 +679,7 @@ static int launch_solve(Params &P, const Layout &L, const unsigned long long *d_
     HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
     HC_CUDA_TRY(cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)n, st));  // every live list: not scanned yet
     void *args[] = {&P};
-    x8 = x8 && narrow && d_stats == nullptr && !live;  // (the instantiations select_kernel has)
+    x8 = x8 && narrow && d_stats == nullptr && !live && !small;  // (the instantiations select_kernel has)
     const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr, small, plain, ell, live, x8);
     const size_t xbytes = (size_t)n * (x8 ? 1 : x16 && narrow ? 2 : 4);
     const int per_sm = occupancy_of(fn);
@@ -730,7 +728,7 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
         if (rc != HC_OK) return rc;
         HC_CUDA_TRY(cudaStreamSynchronize(st));
         const unsigned overflow = (unsigned)(info[2] & 0xffffffffLL);
-        if (x8 && overflow && pr.narrow && !d_stats && !live_for(ch, mode)) {
+        if (x8 && overflow && pr.narrow && !d_stats && !live_for(ch, mode) && !ch.small) {
             x8 = false;  // redo with 16-bit state words
             continue;
         }

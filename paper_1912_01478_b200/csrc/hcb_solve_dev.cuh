@@ -592,18 +592,13 @@ using LF32 = Fmt<unsigned, int, false, false, false, false, true>;
 using LF16 = Fmt<unsigned short, int, false, false, false, false, true>;
 using LF16D = Fmt<unsigned short, short, false, false, false, false, true>;
 using LF32D = Fmt<unsigned, short, false, false, false, false, true>;
-// 8-bit state words (colors <= 127): graphs of max degree <= 128 (ER-2^25,
-// grids); the whole state array stays L2-resident at twice the node count
+// 8-bit state words (colors <= 127): general-kernel graphs of max degree
+// <= 128 (ER-2^25): the whole state array stays L2-resident at twice the node
+// count.  (Bin-0-only graphs keep 16 bits: grid4096 measured 352 -> 355 ms.)
 using F8 = Fmt<unsigned char, int>;
 using F8D = Fmt<unsigned char, short>;
-using SF8 = Fmt<unsigned char, int, false, true>;
-using SF8D = Fmt<unsigned char, short, false, true>;
-using SEF8D = Fmt<unsigned char, short, false, true, false, true>;
 using PF8 = Fmt<unsigned char, int, false, false, true>;
 using PF8D = Fmt<unsigned char, short, false, false, true>;
-using PSF8 = Fmt<unsigned char, int, false, true, true>;
-using PSF8D = Fmt<unsigned char, short, false, true, true>;
-using PSEF8D = Fmt<unsigned char, short, false, true, true, true>;
 
 // committed flag / color mask of the format's state word; words are kept
 // zero-extended in registers, so no conversion on load or store
@@ -2507,11 +2502,10 @@ const void *kernel_ptr() {
     X(int, PSEF32D, false)
 #define HC_INST_G9(X) HC_SIX(X, L, false)
 #define HC_INST_G10(X) HC_SIX(X, L, true)
-#define HC_INST_G11(X) X(int, F8, false) X(int, F8D, false) X(int, SF8, false) X(int, SF8D, false) X(int, SEF8D, false)
-#define HC_INST_G12(X) X(int, PF8, false) X(int, PF8D, false) X(int, PSF8, false) X(int, PSF8D, false) X(int, PSEF8D, false)
+#define HC_INST_G11(X) X(int, F8, false) X(int, F8D, false) X(int, PF8, false) X(int, PF8D, false)
 #define HC_INST_ALL(X) \
     HC_INST_G0(X) HC_INST_G1(X) HC_INST_G2(X) HC_INST_G3(X) HC_INST_G4(X) HC_INST_G5(X) HC_INST_G6(X) HC_INST_G7(X) \
-    HC_INST_G8(X) HC_INST_G9(X) HC_INST_G10(X) HC_INST_G11(X) HC_INST_G12(X)
+    HC_INST_G8(X) HC_INST_G9(X) HC_INST_G10(X) HC_INST_G11(X)
 
 }  // namespace solve
 }  // namespace hcb

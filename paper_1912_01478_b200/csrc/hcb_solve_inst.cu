@@ -1,9 +1,9 @@
 // hcb_solve_inst.cu -- explicit solve_kernel instantiations, one group per
-// object (make builds it with -DHC_INST_GROUP=0..12 in parallel).
+// object (make builds it with -DHC_INST_GROUP=0..11 in parallel).
 #include "hcb_solve_dev.cuh"
 
 #ifndef HC_INST_GROUP
-#error "compile with -DHC_INST_GROUP=<0..12>"
+#error "compile with -DHC_INST_GROUP=<0..11>"
 #endif
 #define HC_CAT2(a, b) a##b
 #define HC_CAT(a, b) HC_CAT2(a, b)

@@ -308,8 +308,8 @@ def test_forced_storage_formats_vs_golden(configs, fmt):
 @pytest.mark.parametrize("x8", [1, 0])
 def test_8bit_state_words_vs_oracle(x8):
     """8-bit state words (every degree <= 128) against the oracle, and with
-    them forbidden: ER graphs of max degree ~60-110, a grid (the ELL4 and
-    bin-0-only kernels), and cliques K_128 / K_129 whose last tentative colors
+    them forbidden: ER graphs of max degree ~60-110, a grid (bin-0-only: keeps
+    16-bit words either way), and cliques K_128 / K_129 whose last tentative colors
     (128, 129) overflow 8 bits, so the solve is redone with 16-bit words."""
     L = hc._lib.load()
     L.hc_solve_set_x8(x8)
