@@ -686,7 +686,11 @@ static int launch_solve(Params &P, const Layout &L, const unsigned long long *d_
     HC_REQUIRE(per_sm > 0, HC_ERR_CUDA, "hc_solve: occupancy query failed");
     P.nblocks = (unsigned)(per_sm * std::max(1, num_sms()));
     bool windowed = false;
-    HC_CUDA_TRY(launch_persistent(fn, P.nblocks, args, st, P.X, xbytes, true, &windowed));
+    // the L2 window pays on bin-0-only graphs (grid4096: 464 -> 443 ms); with
+    // 8-bit words ER-2^25's 33.5 MB array would qualify too, but measured
+    // 46.6 -> 50.1 ms with it (its gathers already hit; the set-aside shrinks
+    // the L2 left to the column and list streams)
+    HC_CUDA_TRY(launch_persistent(fn, P.nblocks, args, st, P.X, small ? xbytes : 0, true, &windowed));
     // the persisting lines go back to normal: nothing of this solve stays
     // pinned in L2 for the caller's next kernel (or the next solve)
     if (windowed) HC_CUDA_TRY(l2_demote(P.X, xbytes, st));
