@@ -151,8 +151,8 @@ int hc_solve_set_x8(int allow);
  * >= 2^25 half-edges), 0 = off, 1 = on (per calling host thread). */
 int hc_solve_set_live(int mode);
 /* L2 residency of the state words (per calling host thread).  When the
- * state-word array is 16 MB .. L2/3 (grids and meshes of ~8-40 M nodes)
- * hc_solve launches the solve kernel with the array as a persisting
+ * state-word array is 16 MB .. L2/3 and the graph is bin-0-only (every
+ * degree <= 16: grids and meshes of ~8-40 M nodes) hc_solve launches the solve kernel with the array as a persisting
  * access-policy window and sets the device's persisting set-aside
  * (cudaLimitPersistingL2CacheSize, a device-wide limit) to exactly its
  * size; after the solve a stream-ordered pass demotes those lines to normal
