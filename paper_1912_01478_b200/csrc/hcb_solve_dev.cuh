@@ -752,10 +752,13 @@ __device__ __forceinline__ void fb_or(unsigned *a, unsigned bits) {
 
 // winner's color c into neighbour v's bitmap (fire-and-forget RED).
 // CHECK: v's word was not read yet -- with HC_FB_FILTER a committed v (whose
-// bitmap is never read again) gets no push
+// bitmap is never read again) gets no push.  Not in the bin-0-only kernel:
+// there a winner has at most a few unread (higher) neighbours and the
+// dependent gather costs more than the extra REDs (grid4096 353.7 -> 350.1
+// ms without it; ER-2^25 needs it: 46.6 vs 55.2 ms)
 template <class F, bool CHECK = true, typename OffT>
 __device__ __forceinline__ void fb_push(const Params &P, const OffT *ro, int v, unsigned c) {
-    if constexpr (CHECK && HC_FB_FILTER) {
+    if constexpr (CHECK && HC_FB_FILTER && !F::small) {
         if (xget<F>(P, v) & FB<F>) return;
     }
     if (c <= 32u) {
