@@ -22,6 +22,14 @@ for scale in (8, 10):
     _L0.load().hc_solve_set_live(-1)
 dg = hc.grid_graph(40, 30)
 c, rep = hc.color_graph(dg)
+# 8-bit state words (every degree <= 128), and their overflow rerun (K_128)
+ro, ci = O.build_csr(2000, O.gen_er(2000, 2000 * 30, 3))
+c, rep = hc.color_graph(hc.CsrGraph(2000, len(ci), ro, ci).to_device())
+assert np.array_equal(c, O.color(ro, ci, "hybrid")[0])
+iu, ju = np.triu_indices(128, 1)
+ro, ci = O.build_csr(128, np.stack([iu, ju], 1).astype(np.int64))
+c, rep = hc.color_graph(hc.CsrGraph(128, len(ci), ro, ci).to_device())
+assert np.array_equal(c, O.color(ro, ci, "hybrid")[0])
 # star hub (bin 4, split slices) + per-round plugin API + worklist sort
 n = 6000
 e = np.concatenate([np.column_stack([np.zeros(n - 1, np.int64), np.arange(1, n)]),
