@@ -273,8 +273,18 @@ static const void *select_kernel_mg(bool narrow, bool x16, bool c16, bool small 
 }
 
 static int occupancy_of(const void *fn) {
+    // cached per (kernel, device, calling thread): the query costs host time
+    // on every solve, while the GPU waits for the launch (small graphs)
+    static thread_local std::unordered_map<const void *, int> cache[8];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = -1;
+    if (dev >= 0 && dev < 8) {
+        const auto it = cache[dev].find(fn);
+        if (it != cache[dev].end()) return it->second;
+    }
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, BLOCK, 0) != cudaSuccess) return 0;
+    if (dev >= 0 && dev < 8) cache[dev][fn] = per_sm;
     return per_sm;
 }
 
@@ -669,21 +679,35 @@ static Choice choose(const Prep &pr, long long m) {
 // (pure topology sweeps read the static rows and measured faster without live lists)
 static bool live_for(const Choice &c, int mode) { return c.live_ok && (g_live == 1 || mode != HC_MODE_TOPO); }
 
+// the forbidden-color extension words (fb0 is zeroed by the kernel) and the
+// live-list counts (-1: not scanned yet) of a solve
+static cudaError_t reset_solve_buffers(const Params &P, const Layout &L, long long n, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)n, st);
+    return e;
+}
+
 // stream-ordered reset of the per-solve state and the cooperative launch
 // (no host synchronisation); info_dst: where the (rounds, record overflow /
 // stall, format overflow) triple is copied (host for hc_solve, device for
 // hc_solve_launch)
 static int launch_solve(Params &P, const Layout &L, const unsigned long long *d_totals, long long n, bool narrow,
                         bool x16, bool c16, bool small, bool ell, bool live, bool plain, int64_t *d_stats,
-                        void *info_dst, cudaMemcpyKind info_kind, cudaStream_t st, bool x8 = false) {
-    HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
-    copy_totals_kernel<<<1, 32, 0, st>>>(d_totals, P.ctrl);
-    HC_CHECK_LAUNCH();
-    HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
+                        void *info_dst, cudaMemcpyKind info_kind, cudaStream_t st, bool x8 = false,
+                        bool fresh = false) {
+    // fresh: hc_solve's first launch -- prepare() has just reset the control
+    // block and the hub slots and copied the totals, and the bitmap / live
+    // count resets were queued before its sync (reset_solve_buffers), so
+    // nothing but the launch is issued after the host sync
+    if (!fresh) {
+        HC_CUDA_TRY(cudaMemsetAsync(P.ctrl, 0, offsetof(Ctrl, segcnt), st));
+        copy_totals_kernel<<<1, 32, 0, st>>>(d_totals, P.ctrl);
+        HC_CHECK_LAUNCH();
+        HC_CUDA_TRY(cudaMemsetAsync(P.hub_acc, 0, sizeof(HubAcc) * MAX_SPLIT_SLOTS, st));
+        HC_CUDA_TRY(reset_solve_buffers(P, L, n, st));
+    }
     if (d_stats && P.max_rec)
         HC_CUDA_TRY(cudaMemsetAsync(d_stats, 0, sizeof(int64_t) * 2 * (size_t)P.max_rec, st));
-    HC_CUDA_TRY(cudaMemsetAsync(P.fbx, 0, L.fbx_bytes, st));  // fb0 is zeroed by the kernel
-    HC_CUDA_TRY(cudaMemsetAsync(P.lcnt, 0xff, 4 * (size_t)n, st));  // every live list: not scanned yet
     void *args[] = {&P};
     x8 = x8 && narrow && d_stats == nullptr && !live && !small;  // (the instantiations select_kernel has)
     const void *fn = select_kernel(narrow, x16, c16, d_stats != nullptr, small, plain, ell, live, x8);
@@ -726,15 +750,17 @@ static int solve_impl(const int64_t *d_row_offsets, const int32_t *d_col_indices
     Params P{};
     init_solve(P, L, ws, d_col_indices, num_nodes, mode, thr_count, d_colors, d_rec, max_rec, d_stats);
     Prep pr;
+    HC_CUDA_TRY(reset_solve_buffers(P, L, num_nodes, st));  // (queued ahead of prepare's sync)
     int rc = prepare(P, L, ws, d_row_offsets, num_nodes, num_edges, false, pr, st,
                      reinterpret_cast<unsigned long long *>(ws + L.ell));
     if (rc != HC_OK) return rc;
     const Choice ch = choose(pr, num_edges);
-    bool x16 = ch.x16, x8 = ch.x8;
+    bool x16 = ch.x16, x8 = ch.x8, fresh = true;
     long long info[3];
     for (;;) {
         rc = launch_solve(P, L, pr.d_totals, num_nodes, pr.narrow, x16, ch.c16, ch.small, ch.ell, live_for(ch, mode),
-                          plain, d_stats, info, cudaMemcpyDeviceToHost, st, x8);
+                          plain, d_stats, info, cudaMemcpyDeviceToHost, st, x8, fresh);
+        fresh = false;  // a rerun resets everything again
         if (rc != HC_OK) return rc;
         HC_CUDA_TRY(cudaStreamSynchronize(st));
         const unsigned overflow = (unsigned)(info[2] & 0xffffffffLL);
