@@ -2274,27 +2274,31 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             rc.csz[1] = chunk_size(rc.L[1].total, NW * 4);
             rc.csz[2] = chunk_size(rc.L[2].total, NW * 2);
             rc.csz[3] = (bin3_cta && rc.L[3].total <= MAXSEG) ? 1u : chunk_size(rc.L[3].total, NW);
+            // (32-bit divisions: list totals are < 2^31, and thread 0's
+            // arithmetic here is on every round's critical path)
             for (int b = 0; b < NSEG_BINS; ++b)
-                rc.nch[b] = (unsigned)((rc.L[b].total + rc.csz[b] - 1) / rc.csz[b]);
+                rc.nch[b] = ((unsigned)rc.L[b].total + rc.csz[b] - 1u) / rc.csz[b];
             rc.bin3_by_cta = rc.csz[3] == 1u;
             // group-bin work units: whole warp tiles, about UPC per CTA at most;
             // bin 3 (degrees 65..4096) keeps one tile per unit up to 64 per CTA
+#pragma unroll
             for (int b = 1; b < NSEG_BINS; ++b) {
                 // bins 1, 2 (similar degrees): unit = segment; bin 3 (65..4096):
                 // about HC_UPC3 units per CTA, at least one warp tile each
                 const unsigned tile = NW * (b == 1 ? 4u : b == 2 ? 2u : 1u);
-                const unsigned long long tiles = (rc.L[b].total + tile - 1) / tile;
-                unsigned long long k = b == 3 ? tiles / ((unsigned long long)HC_UPC3 * P.nblocks) : ~0ull;
-                k = max(1ull, min(k, (unsigned long long)(rc.csz[b] / tile)));
-                rc.su[b] = (b == 3 && rc.bin3_by_cta) ? 1u : (unsigned)(k * tile);
-                rc.nsu[b] = (unsigned)((rc.L[b].total + rc.su[b] - 1) / rc.su[b]);
+                const unsigned tot = (unsigned)rc.L[b].total;
+                const unsigned tiles = (tot + tile - 1u) / tile;
+                unsigned k = b == 3 ? tiles / ((unsigned)HC_UPC3 * P.nblocks) : ~0u;
+                k = max(1u, min(k, rc.csz[b] / tile));
+                rc.su[b] = (b == 3 && rc.bin3_by_cta) ? 1u : k * tile;
+                rc.nsu[b] = (tot + rc.su[b] - 1u) / rc.su[b];
             }
             // the heaviest bin-3 nodes (list front) one CTA each: a single
             // degree-4096 node would hold a warp ~28 us (RMAT-16 resolve)
             rc.k3 = rc.bin3_by_cta ? (unsigned)rc.L[3].total
                                    : (unsigned)min(rc.L[3].total, (unsigned long long)(P.nblocks * HC_K3 / 100));
             if (!rc.bin3_by_cta)
-                rc.nsu[3] = (unsigned)((rc.L[3].total - rc.k3 + rc.su[3] - 1) / rc.su[3]);
+                rc.nsu[3] = ((unsigned)rc.L[3].total - rc.k3 + rc.su[3] - 1u) / rc.su[3];
             else
                 rc.nsu[3] = 0;
             const bool live = s != 0;
