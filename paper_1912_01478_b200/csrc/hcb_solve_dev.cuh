@@ -2406,10 +2406,19 @@ __global__ void __launch_bounds__(BLOCK, F::small ? MIN_CTAS_SMALL : MIN_CTAS) s
             }
             if (threadIdx.x == 0) sm.hub_pre[0] = 0;
             __syncthreads();
-            if (threadIdx.x == 0) {  // H < nblocks <= a few hundred: serial scan
-                for (unsigned i = 1; i <= H; ++i) sm.hub_pre[i] += sm.hub_pre[i - 1];
-                const unsigned extra = sm.hub_pre[H] - H;
-                for (int b = 1; b <= NBIN; ++b) rc.ubase[b] += extra;
+            if (warp == 0) {  // H < nblocks <= a few hundred: warp scan, 32 slots per step
+                unsigned carry = 0;
+                for (unsigned i0 = 1; i0 <= H; i0 += 32) {
+                    const unsigned i = i0 + lane;
+                    const unsigned v = i <= H ? sm.hub_pre[i] : 0u;
+                    const unsigned incl = warp_incl_scan(v) + carry;
+                    if (i <= H) sm.hub_pre[i] = incl;
+                    carry = __shfl_sync(FULL, incl, 31);
+                }
+                if (lane == 0) {
+                    const unsigned extra = carry - H;
+                    for (int b = 1; b <= NBIN; ++b) rc.ubase[b] += extra;
+                }
             }
             __syncthreads();
         }
