@@ -123,6 +123,9 @@ struct GridBarrier {
 #ifndef HC_FAST_BARRIER
 #define HC_FAST_BARRIER 1
 #endif
+#ifndef HC_BAR_SLEEP
+#define HC_BAR_SLEEP 20  // ns between polls of the barrier generation
+#endif
 __device__ __forceinline__ void grid_sync(GridBarrier *b, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -138,7 +141,7 @@ __device__ __forceinline__ void grid_sync(GridBarrier *b, unsigned nblocks) {
             asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(&b->count), "r"(0u) : "memory");
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&b->gen), "r"(g + 1u) : "memory");
         } else {
-            while (ld_acquire_u32(&b->gen) == g) __nanosleep(20);
+            while (ld_acquire_u32(&b->gen) == g) __nanosleep(HC_BAR_SLEEP);
         }
 #else
         unsigned g = ld_acquire_u32(&b->gen);
