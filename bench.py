@@ -622,7 +622,7 @@ def run_ours(args, cfg):
         for name in CONFIGS:
             if name == args.config:
                 continue
-            line["configs"][name] = measure(args, name, min(args.steps, 5), 3, e2e_steps=2,
+            line["configs"][name] = measure(args, name, min(args.steps, 5), 3, e2e_steps=3,
                                             mode_reps=2 if name == "rmat26" else 3,
                                             cpu_budget=args.cpu_budget_configs)
             line["gpu_launches"] += line["configs"][name]["gpu_launches"]
