@@ -21,6 +21,7 @@ import ctypes
 import json
 import math
 from dataclasses import dataclass, field
+from types import SimpleNamespace
 from typing import IO
 
 import numpy as np
@@ -143,7 +144,14 @@ class Solver:
 
     def __init__(self, graph: DeviceCsr, max_rec: int | None = None):
         self.L = _lib.load()
-        self.g = graph.ensure_lower_first()
+        # the solver keeps the graph's tensors, not the DeviceCsr: color_graph
+        # caches the solver on the DeviceCsr, and a graph -> solver -> graph
+        # cycle kept a dropped graph's CSR and workspace on the GPU until the
+        # cyclic GC ran (later calls then allocated afresh: e2e steps 370 ms
+        # one time, 400+ the next)
+        lf = graph.ensure_lower_first()
+        self.g = SimpleNamespace(num_nodes=lf.num_nodes, num_edges=lf.num_edges, row_offsets=lf.row_offsets,
+                                 col_indices=lf.col_indices, device=lf.device)
         dev = graph.device
         n = graph.num_nodes
         self.ws = _lib.workspace(self.L.hc_solve_workspace_bytes(n, graph.num_edges), dev)
