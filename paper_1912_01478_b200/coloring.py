@@ -47,7 +47,9 @@ def _device_graph(graph) -> DeviceCsr:
         # the device copy with it, so per-round calls do no H2D traffic
         dg = graph.__dict__.get("_device_csr")
         if dg is None:
-            dg = graph.__dict__["_device_csr"] = graph.to_device()
+            dg = graph.to_device()
+            dg.host = None  # no host <-> device cycle: the copy goes with the host graph
+            graph.__dict__["_device_csr"] = dg
         graph = dg
     if not isinstance(graph, DeviceCsr):
         raise TypeError("expected CsrGraph or DeviceCsr")
