@@ -9,7 +9,7 @@ k = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 dg = hc.grid_graph(k, k)
 host = hc.CsrGraph.pinned(dg.to_host())
 cfg = hc.HybridConfig()
-for it in range(4):
+for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 4):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     d2 = host.to_device(); torch.cuda.synchronize(); t1 = time.perf_counter()
     s = hc.Solver(d2); torch.cuda.synchronize(); t2 = time.perf_counter()
