@@ -1610,7 +1610,7 @@ __device__ __forceinline__ void group_sub(const Params &P, const OffT *ro, Smem 
         for (; v0 < hi; v0 += STEP) {  // warp-uniform
             GEntry nxt{-1, 0u, 0ull};
             if (v0 + STEP < hi) nxt = group_fetch<G, F, PHASE>(P, rc.L[bin], sm.prefix[bin], v0 + STEP, hi, rc.topo, seg);
-            const unsigned c = (unsigned)(v0 / csz);  // a warp tile never straddles segments (csz: whole tiles)
+            const unsigned c = (unsigned)v0 / csz;  // a warp tile never straddles segments (csz: whole tiles); 32-bit: positions < 2^31
             group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo,
                                               dyn_list(P, np, bin) + (long long)c * csz,
                                               dyn_od(P, np, bin) + (long long)c * csz,
@@ -1620,7 +1620,7 @@ __device__ __forceinline__ void group_sub(const Params &P, const OffT *ro, Smem 
         }
     } else {
         for (unsigned long long v0 = lo + (unsigned long long)warp * NG; v0 < hi; v0 += STEP) {
-            const unsigned c = (unsigned)(v0 / csz);  // a warp tile never straddles segments (csz: whole tiles)
+            const unsigned c = (unsigned)v0 / csz;  // a warp tile never straddles segments (csz: whole tiles); 32-bit: positions < 2^31
             group_tile<G, OffT, F, STATS, PHASE>(P, ro, rc.L[bin], sm.prefix[bin], v0, hi, rc.topo,
                                               dyn_list(P, np, bin) + (long long)c * csz,
                                               dyn_od(P, np, bin) + (long long)c * csz,
