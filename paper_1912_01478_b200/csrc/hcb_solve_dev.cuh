@@ -1142,21 +1142,26 @@ __device__ __forceinline__ void group_tile(const Params &P, const OffT *ro, cons
         if constexpr (FBM<F>) {
             if (u >= 0 && cnt == 0) {  // group-uniform: the winner's color goes into every neighbour's bitmap
                 if constexpr (G < 32) {
+                    // the committed-neighbour filter's word loads are issued
+                    // together, before any RED (a RED between them would order
+                    // the next load behind it: four dependent round trips)
+                    int w[4];
                     if (lsrc) {  // nb held the live lower list: the whole row comes from the columns
-                        int w[4];
 #pragma unroll
                         for (int q = 0; q < 4; ++q) {
                             const long long k = b + sub + q * G;
                             w[q] = k < e ? colget<F>(P, k, u) : -1;
                         }
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (w[q] >= 0) fb_push<F>(P, ro, w[q], xu);
                     } else {  // the first column batch is the whole adjacency
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (nb[q] != 0x7fffffff) fb_push<F>(P, ro, nb[q], xu);
+                        for (int q = 0; q < 4; ++q) w[q] = nb[q] != 0x7fffffff ? nb[q] : -1;
                     }
+                    unsigned xw[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) xw[q] = (HC_FB_FILTER && w[q] >= 0) ? xget<F>(P, w[q]) : 0u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (w[q] >= 0 && !(xw[q] & FB<F>)) fb_push<F, false>(P, ro, w[q], xu);
                 } else {  // whole warp, one node: PU column loads per lane in flight
                     for (long long k0 = b + sub; k0 < e; k0 += (long long)PU * G) {
                         int w[PU];
