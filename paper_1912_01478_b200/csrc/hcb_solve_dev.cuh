@@ -1558,19 +1558,42 @@ __device__ __forceinline__ void tile_finish(const Params &P, const OffT *ro, con
             for (int j = 0; j < NP; ++j) {
                 if (u[j] < 0 || lost[j]) continue;
                 const unsigned T = xu[j];
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (nb[j][q] >= 0 && !(nb[j][q] < u[j] && (x[j][q] & FB<F>))) {
-                        if (nb[j][q] < u[j]) fb_push<F, false>(P, ro, nb[j][q], T);  // word already read
-                        else fb_push<F>(P, ro, nb[j][q], T);
-                    }
-                for (OffT k = rb[j] + 4; !F::ell && k < re[j]; k += 4) {  // deg 5..16
-                    int v2[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? colget<F>(P, k + q, u[j]) : -1;
+                if constexpr (F::small) {  // (no filter loads: the original order measured faster on the grid)
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        if (v2[q] >= 0) fb_push<F>(P, ro, v2[q], T);
+                        if (nb[j][q] >= 0 && !(nb[j][q] < u[j] && (x[j][q] & FB<F>))) {
+                            if (nb[j][q] < u[j]) fb_push<F, false>(P, ro, nb[j][q], T);  // word already read
+                            else fb_push<F>(P, ro, nb[j][q], T);
+                        }
+                    for (OffT k = rb[j] + 4; !F::ell && k < re[j]; k += 4) {  // deg 5..16
+                        int v2[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? colget<F>(P, k + q, u[j]) : -1;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (v2[q] >= 0) fb_push<F>(P, ro, v2[q], T);
+                    }
+                } else {
+                    // the filter's word loads before any RED: a RED between
+                    // them would order each load behind the last RED
+                    unsigned xw[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)  // a lower neighbour's word was already read
+                        xw[q] = nb[j][q] < 0 ? FB<F> : nb[j][q] < u[j] ? x[j][q] : HC_FB_FILTER ? xget<F>(P, nb[j][q]) : 0u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (!(xw[q] & FB<F>)) fb_push<F, false>(P, ro, nb[j][q], T);
+                    for (OffT k = rb[j] + 4; k < re[j]; k += 4) {  // deg 5..16
+                        int v2[4];
+                        unsigned x2[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) v2[q] = k + q < re[j] ? colget<F>(P, k + q, u[j]) : -1;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) x2[q] = v2[q] < 0 ? FB<F> : HC_FB_FILTER ? xget<F>(P, v2[q]) : 0u;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (!(x2[q] & FB<F>)) fb_push<F, false>(P, ro, v2[q], T);
+                    }
                 }
             }
         }
